@@ -1,0 +1,400 @@
+/*
+ * oracle.c — CPU ORACLE for per-edge triangle support, triangle count and
+ * k-truss (Samsi et al., "Static Graph Challenge: Subgraph Isomorphism",
+ * arXiv 1708.06866; cited as P:<line> of PAPER.md).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.  The
+ * product path (paper_1708_06866_b200/, libgc.so) never links, loads or
+ * calls it, and this file shares no code, header, table or constant with it.
+ *
+ * Plain, slow and obviously correct: each function writes out a definition
+ * from the paper (or, where the paper gives an array algorithm, its
+ * element-wise meaning) with no blocking or reordering beyond it.  Integer
+ * results are independent of the thread count (threads take static chunks
+ * of independent edges and only write their own outputs).
+ *
+ *   O-1  or_canonicalize      self loops removed, reverse edges added,
+ *                             duplicates dropped (reading A1)
+ *   O-2  or_adjacency         N(x) sorted ascending, with edge ids
+ *   O-3  or_support           support(a,b) = |N(a) ∩ N(b)|  (P:283-288:
+ *                             "the overlap of the neighborhoods")
+ *   O-4  or_triangle_count    #{a<b<w pairwise adjacent}
+ *   O-5  or_ktruss            Alg. 4 batch semantics: repeat
+ *                             { recompute s on the alive subgraph;
+ *                               x = {s < k-2}; drop x } until x is empty
+ *   O-6  or_truss_decomposition  P:299-302: k = 3, 4, ... each from the
+ *                             previous result until empty
+ *   O-7  or_truss_sequential  tier 2: one-edge-at-a-time min-support peel
+ *                             (bucket order); equal to O-6 by uniqueness
+ *                             of the maximal k-truss (reading A2/A8)
+ *
+ * Pins: tests/test_oracle_pins.py (brute force, closed forms, trace(A^3)/6,
+ * literal Alg. 1-4 in scipy, networkx, Table II, invariants).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+#include <unistd.h>
+
+static int n_threads(int t) {
+    if (t > 0) return t;
+    long c = sysconf(_SC_NPROCESSORS_ONLN);
+    if (c < 1) c = 1;
+    if (c > 256) c = 256;
+    return (int)c;
+}
+
+/* Run fn(ctx, i0, i1, t) over [0, N) in T static chunks (chunk t). */
+typedef void (*range_fn)(void* ctx, int64_t i0, int64_t i1, int t);
+typedef struct { range_fn fn; void* ctx; int64_t i0, i1; int t; } range_job;
+static void* range_tramp(void* a) { range_job* j = (range_job*)a; j->fn(j->ctx, j->i0, j->i1, j->t); return NULL; }
+static void parallel_for(int64_t N, int T, range_fn fn, void* ctx) {
+    T = n_threads(T);
+    if (N < 1024 || T == 1) { fn(ctx, 0, N, 0); return; }
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * T);
+    range_job* jb = (range_job*)malloc(sizeof(range_job) * T);
+    for (int t = 0; t < T; ++t) {
+        jb[t].fn = fn; jb[t].ctx = ctx; jb[t].i0 = N * t / T; jb[t].i1 = N * (t + 1) / T; jb[t].t = t;
+        pthread_create(&th[t], NULL, range_tramp, &jb[t]);
+    }
+    for (int t = 0; t < T; ++t) pthread_join(th[t], NULL);
+    free(th); free(jb);
+}
+
+/* ------------------------------------------------------------ sorting --
+ * LSD radix sort of uint64 keys, one byte per pass (a library-primitive
+ * sort; pinned against numpy.sort in the tests). */
+int or_sort_u64(uint64_t* keys, int64_t N) {
+    if (N <= 1) return 0;
+    uint64_t* tmp = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)N);
+    if (!tmp) return -1;
+    uint64_t* src = keys; uint64_t* dst = tmp;
+    for (int pass = 0; pass < 8; ++pass) {
+        int sh = 8 * pass;
+        int64_t cnt[256];
+        memset(cnt, 0, sizeof(cnt));
+        for (int64_t i = 0; i < N; ++i) cnt[(src[i] >> sh) & 0xFF]++;
+        if (cnt[(src[0] >> sh) & 0xFF] == N) continue;   /* byte constant: pass is identity */
+        int64_t off = 0;
+        for (int d = 0; d < 256; ++d) { int64_t c = cnt[d]; cnt[d] = off; off += c; }
+        for (int64_t i = 0; i < N; ++i) dst[cnt[(src[i] >> sh) & 0xFF]++] = src[i];
+        uint64_t* t = src; src = dst; dst = t;
+    }
+    if (src != keys) memcpy(keys, src, sizeof(uint64_t) * (size_t)N);
+    free(tmp);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ O-1 --
+ * Canonical edge list (SURVEY §8(b) "Edge order / ids"):
+ * drop u == v, orient (min, max), sort lexicographically, drop duplicates.
+ * Edge id = position.  n = max raw id + 1 (0 if nnz == 0).
+ * cu, cv: capacity nnz.  Returns m, or -1 on a negative id / OOM. */
+int64_t or_canonicalize(const int32_t* u, const int32_t* v, int64_t nnz,
+                        int32_t* cu, int32_t* cv, int64_t* n_out) {
+    int64_t maxid = -1;
+    for (int64_t i = 0; i < nnz; ++i) {
+        if (u[i] < 0 || v[i] < 0) return -1;
+        if (u[i] > maxid) maxid = u[i];
+        if (v[i] > maxid) maxid = v[i];
+    }
+    *n_out = maxid + 1;
+    uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nnz > 0 ? nnz : 1));
+    if (!keys) return -1;
+    int64_t k = 0;
+    for (int64_t i = 0; i < nnz; ++i) {
+        if (u[i] == v[i]) continue;                            /* self loop removed */
+        uint32_t a = (uint32_t)(u[i] < v[i] ? u[i] : v[i]);    /* both orientations -> one */
+        uint32_t b = (uint32_t)(u[i] < v[i] ? v[i] : u[i]);
+        keys[k++] = ((uint64_t)a << 32) | b;
+    }
+    if (or_sort_u64(keys, k) != 0) { free(keys); return -1; }
+    int64_t m = 0;
+    for (int64_t i = 0; i < k; ++i) {
+        if (i > 0 && keys[i] == keys[i - 1]) continue;         /* duplicate dropped */
+        cu[m] = (int32_t)(keys[i] >> 32);
+        cv[m] = (int32_t)(keys[i] & 0xFFFFFFFFULL);
+        ++m;
+    }
+    free(keys);
+    return m;
+}
+
+/* ------------------------------------------------------------------ O-2 --
+ * Symmetric adjacency: row x lists N(x) ascending with the canonical id of
+ * each edge.  Filling rows while scanning the lexicographic edge list puts
+ * lower neighbours (edges (w,x), w<x) before upper ones (edges (x,w), x<w),
+ * each ascending, so rows come out sorted.
+ * ptr: n+1, col/eid: 2m. */
+void or_adjacency(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
+                  int64_t* ptr, int32_t* col, int32_t* eid) {
+    for (int64_t x = 0; x <= n; ++x) ptr[x] = 0;
+    for (int64_t e = 0; e < m; ++e) { ptr[cu[e] + 1]++; ptr[cv[e] + 1]++; }
+    for (int64_t x = 0; x < n; ++x) ptr[x + 1] += ptr[x];
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t x = 0; x < n; ++x) fill[x] = ptr[x];
+    for (int64_t e = 0; e < m; ++e) {
+        int32_t a = cu[e], b = cv[e];
+        col[fill[a]] = b; eid[fill[a]] = (int32_t)e; fill[a]++;
+        col[fill[b]] = a; eid[fill[b]] = (int32_t)e; fill[b]++;
+    }
+    free(fill);
+}
+
+/* Sorted-list intersection |A ∩ B| by two-pointer merge; when one list is at
+ * least 32x longer, each element of the short list is located in the long
+ * one by binary search instead (same set, fewer steps). */
+static int64_t lower_bound32(const int32_t* a, int64_t lo, int64_t hi, int32_t x) {
+    while (lo < hi) { int64_t mid = lo + (hi - lo) / 2; if (a[mid] < x) lo = mid + 1; else hi = mid; }
+    return lo;
+}
+
+static int64_t intersect_count(const int32_t* A, int64_t na, const int32_t* B, int64_t nb) {
+    if (na == 0 || nb == 0) return 0;
+    if (na > nb) { const int32_t* t = A; A = B; B = t; int64_t tn = na; na = nb; nb = tn; }
+    int64_t c = 0;
+    if (nb >= 32 * na) {
+        int64_t lo = 0;
+        for (int64_t i = 0; i < na; ++i) {
+            lo = lower_bound32(B, lo, nb, A[i]);
+            if (lo < nb && B[lo] == A[i]) { ++c; ++lo; }
+        }
+        return c;
+    }
+    int64_t i = 0, j = 0;
+    while (i < na && j < nb) {
+        if (A[i] < B[j]) ++i;
+        else if (A[i] > B[j]) ++j;
+        else { ++c; ++i; ++j; }
+    }
+    return c;
+}
+
+/* ------------------------------------------------------------------ O-3 --
+ * support(a_i, b_i) = |N(a_i) ∩ N(b_i)| for a list of vertex pairs (the
+ * canonical edge list, or a sample of it).  sup: npairs. */
+typedef struct { const int64_t* ptr; const int32_t* col; const int32_t* a; const int32_t* b; uint32_t* sup; } sup_ctx;
+static void sup_range(void* c, int64_t i0, int64_t i1, int t) {
+    (void)t;
+    sup_ctx* C = (sup_ctx*)c;
+    for (int64_t i = i0; i < i1; ++i) {
+        int32_t a = C->a[i], b = C->b[i];
+        C->sup[i] = (uint32_t)intersect_count(C->col + C->ptr[a], C->ptr[a + 1] - C->ptr[a],
+                                              C->col + C->ptr[b], C->ptr[b + 1] - C->ptr[b]);
+    }
+}
+void or_support(const int64_t* ptr, const int32_t* col, int64_t npairs,
+                const int32_t* a, const int32_t* b, uint32_t* sup, int nthreads) {
+    sup_ctx C = {ptr, col, a, b, sup};
+    parallel_for(npairs, nthreads, sup_range, &C);
+}
+
+/* ------------------------------------------------------------------ O-4 --
+ * Triangle count in vertex-id order: each triangle {a<b<w} is counted once,
+ * from its edge (a,b), as a common neighbour w > b (P:159-160 definition).
+ * Independent of any degree orientation. */
+typedef struct { const int64_t* ptr; const int32_t* col; const int32_t* cu; const int32_t* cv; uint64_t* part; } tc_ctx;
+static void tc_range(void* c, int64_t i0, int64_t i1, int t) {
+    tc_ctx* C = (tc_ctx*)c;
+    uint64_t s = 0;
+    for (int64_t e = i0; e < i1; ++e) {
+        int32_t a = C->cu[e], b = C->cv[e];
+        int64_t a0 = C->ptr[a], a1 = C->ptr[a + 1], b0 = C->ptr[b], b1 = C->ptr[b + 1];
+        int64_t pa = lower_bound32(C->col, a0, a1, b + 1);       /* w > b in N(a) */
+        int64_t pb = lower_bound32(C->col, b0, b1, b + 1);       /* w > b in N(b) */
+        s += (uint64_t)intersect_count(C->col + pa, a1 - pa, C->col + pb, b1 - pb);
+    }
+    C->part[t] = s;
+}
+uint64_t or_triangle_count(const int64_t* ptr, const int32_t* col, int64_t m,
+                           const int32_t* cu, const int32_t* cv, int nthreads) {
+    int T = n_threads(nthreads);
+    uint64_t* part = (uint64_t*)calloc((size_t)T + 1, sizeof(uint64_t));
+    tc_ctx C = {ptr, col, cu, cv, part};
+    parallel_for(m, T, tc_range, &C);
+    uint64_t s = 0;
+    for (int t = 0; t <= T; ++t) s += part[t];
+    free(part);
+    return s;
+}
+
+/* Support restricted to the alive subgraph: common neighbours w of (a,b)
+ * such that both edges (a,w) and (b,w) are alive.  Merge over full rows. */
+static uint32_t alive_support(const int64_t* ptr, const int32_t* col, const int32_t* eid,
+                              const uint8_t* alive, int32_t a, int32_t b) {
+    int64_t i = ptr[a], i1 = ptr[a + 1], j = ptr[b], j1 = ptr[b + 1];
+    uint32_t c = 0;
+    int64_t na = i1 - i, nb = j1 - j;
+    if (na > nb) { int64_t t; t = i; i = j; j = t; t = i1; i1 = j1; j1 = t; t = na; na = nb; nb = t; }
+    if (nb >= 32 * na) {
+        for (; i < i1; ++i) {
+            int64_t p = lower_bound32(col, j, j1, col[i]);
+            if (p < j1 && col[p] == col[i] && alive[eid[i]] && alive[eid[p]]) ++c;
+        }
+        return c;
+    }
+    while (i < i1 && j < j1) {
+        if (col[i] < col[j]) ++i;
+        else if (col[i] > col[j]) ++j;
+        else { if (alive[eid[i]] && alive[eid[j]]) ++c; ++i; ++j; }
+    }
+    return c;
+}
+
+typedef struct { const int64_t* ptr; const int32_t* col; const int32_t* eid; const int32_t* cu; const int32_t* cv;
+                 const uint8_t* alive; uint32_t* s; } rs_ctx;
+static void rs_range(void* c, int64_t e0, int64_t e1, int t) {
+    (void)t;
+    rs_ctx* C = (rs_ctx*)c;
+    for (int64_t e = e0; e < e1; ++e)
+        C->s[e] = C->alive[e] ? alive_support(C->ptr, C->col, C->eid, C->alive, C->cu[e], C->cv[e]) : 0;
+}
+
+/* One Alg. 4 peel at threshold k, starting from `alive` (updated in place).
+ * Each round recomputes s on the alive subgraph for every alive edge
+ * (s = (R==2)·1 with R = E·A of the alive graph), then
+ * removes x = {alive e : s(e) < k-2} as a batch.
+ * removed_level (optional): set to `level_tag` for edges removed here.
+ * trace (optional, cap trace_cap): |x| per round.  Returns #rounds with
+ * non-empty x. */
+static int64_t peel_batch(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
+                          const int64_t* ptr, const int32_t* col, const int32_t* eid,
+                          int32_t k, uint8_t* alive, uint32_t* s,
+                          int32_t* removed_level, int32_t level_tag,
+                          int64_t* trace, int64_t trace_cap, int64_t trace_base, int nthreads) {
+    (void)n;
+    int64_t rounds = 0;
+    for (;;) {
+        rs_ctx C = {ptr, col, eid, cu, cv, alive, s};
+        parallel_for(m, nthreads, rs_range, &C);
+        int64_t nx = 0;
+        /* x is decided for all edges before any is removed (batch) */
+        for (int64_t e = 0; e < m; ++e)
+            if (alive[e] && (int64_t)s[e] < (int64_t)k - 2) { s[e] = 0xFFFFFFFFu; ++nx; }
+        if (nx == 0) break;
+        for (int64_t e = 0; e < m; ++e)
+            if (alive[e] && s[e] == 0xFFFFFFFFu) {
+                alive[e] = 0;
+                if (removed_level) removed_level[e] = level_tag;
+            }
+        if (trace && trace_base + rounds < trace_cap) trace[trace_base + rounds] = nx;
+        ++rounds;
+    }
+    return rounds;
+}
+
+/* ------------------------------------------------------------------ O-5 --
+ * Maximal k-truss (reading A2), k >= 2.  alive_out: m (1 = kept).
+ * trace: |x| per round (may be NULL).  Returns the number of rounds, or -1
+ * for k < 2 (domain error). */
+int64_t or_ktruss(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
+                  const int64_t* ptr, const int32_t* col, const int32_t* eid,
+                  int32_t k, uint8_t* alive_out, int64_t* trace, int64_t trace_cap, int nthreads) {
+    if (k < 2) return -1;
+    for (int64_t e = 0; e < m; ++e) alive_out[e] = 1;
+    uint32_t* s = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
+    int64_t r = peel_batch(n, m, cu, cv, ptr, col, eid, k, alive_out, s, NULL, 0, trace, trace_cap, 0, nthreads);
+    free(s);
+    return r;
+}
+
+/* ------------------------------------------------------------------ O-6 --
+ * Truss decomposition: run the k-truss with k = 3 on the full
+ * graph, then pass the result to k+1, until empty.  tau(e) = k-1 for edges
+ * removed at level k (so every edge has tau >= 2).  kmax = max tau, 0 when
+ * m == 0 (reading A7).  Returns total rounds. */
+int64_t or_truss_decomposition(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
+                               const int64_t* ptr, const int32_t* col, const int32_t* eid,
+                               int32_t* tau, int32_t* kmax_out, int nthreads) {
+    uint8_t* alive = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
+    uint32_t* s = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
+    for (int64_t e = 0; e < m; ++e) { alive[e] = 1; tau[e] = 2; }
+    int64_t left = m, rounds = 0;
+    int32_t kmax = 0;
+    for (int32_t k = 3; left > 0; ++k) {
+        rounds += peel_batch(n, m, cu, cv, ptr, col, eid, k, alive, s, tau, k - 1, NULL, 0, 0, nthreads);
+        left = 0;
+        for (int64_t e = 0; e < m; ++e) left += alive[e];
+    }
+    for (int64_t e = 0; e < m; ++e) if (tau[e] > kmax) kmax = tau[e];
+    *kmax_out = (m > 0) ? kmax : 0;
+    free(alive); free(s);
+    return rounds;
+}
+
+/* ------------------------------------------------------------------ O-7 --
+ * Tier-2 decomposition: remove one edge at a time, always one of minimum
+ * current support (bin-sort buckets as in Batagelj-Zaversnik k-core).  When
+ * e = (a,b) is removed with current support s, tau(e) = s + 2; every live
+ * triangle (e, f, g) loses e, so f and g each lose one unit of support,
+ * unless already at e's level (they will be removed at the same level).
+ * Sequential removal destroys each triangle exactly once.  Equal to O-6 by
+ * uniqueness of the maximal k-truss.  sup_init: O-3 supports (m). */
+int64_t or_truss_sequential(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
+                            const int64_t* ptr, const int32_t* col, const int32_t* eid,
+                            const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out) {
+    (void)n;
+    if (m == 0) { *kmax_out = 0; return 0; }
+    uint32_t* S = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m);
+    uint32_t smax = 0;
+    for (int64_t e = 0; e < m; ++e) { S[e] = sup_init[e]; if (S[e] > smax) smax = S[e]; }
+    int64_t* bin = (int64_t*)calloc((size_t)smax + 2, sizeof(int64_t));
+    int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
+    int64_t* ord = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
+    uint8_t* alive = (uint8_t*)malloc((size_t)m);
+    for (int64_t e = 0; e < m; ++e) bin[S[e] + 1]++;
+    for (uint32_t s = 0; s <= smax; ++s) bin[s + 1] += bin[s];
+    {
+        int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * ((size_t)smax + 1));
+        for (uint32_t s = 0; s <= smax; ++s) fill[s] = bin[s];
+        for (int64_t e = 0; e < m; ++e) { pos[e] = fill[S[e]]++; ord[pos[e]] = e; }
+        free(fill);
+    }
+    for (int64_t e = 0; e < m; ++e) alive[e] = 1;
+    int32_t kmax = 2;
+    /* bin[s] = first position of bucket s among not-yet-processed slots */
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t e = ord[i];
+        uint32_t se = S[e];
+        tau[e] = (int32_t)se + 2;
+        if (tau[e] > kmax) kmax = tau[e];
+        /* live triangles through e: w in N(a) ∩ N(b) with (a,w), (b,w) alive */
+        int32_t a = cu[e], b = cv[e];
+        int64_t p = ptr[a], p1 = ptr[a + 1], q = ptr[b], q1 = ptr[b + 1];
+        while (p < p1 && q < q1) {
+            if (col[p] < col[q]) ++p;
+            else if (col[p] > col[q]) ++q;
+            else {
+                int64_t f = eid[p], g = eid[q];
+                if (alive[f] && alive[g]) {
+                    int64_t fg[2] = {f, g};
+                    for (int t = 0; t < 2; ++t) {
+                        int64_t h = fg[t];
+                        if (S[h] > se) {
+                            /* move h to the front of its bucket, then shrink it by one */
+                            uint32_t sh = S[h];
+                            int64_t first = bin[sh];
+                            if (first < i + 1) first = i + 1;
+                            int64_t hw = ord[first];
+                            if (hw != h) {
+                                ord[pos[h]] = hw; pos[hw] = pos[h];
+                                ord[first] = h; pos[h] = first;
+                            }
+                            bin[sh] = first + 1;
+                            S[h] = sh - 1;
+                        }
+                    }
+                }
+                ++p; ++q;
+            }
+        }
+        alive[e] = 0;
+        /* buckets below the next slot are exhausted */
+        if (bin[se] < i + 1) bin[se] = i + 1;
+    }
+    *kmax_out = kmax;
+    free(S); free(bin); free(pos); free(ord); free(alive);
+    return m;
+}
