@@ -33,7 +33,7 @@ build/%.o: $(CSRC)/%.cu $(GC_HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.txt || (cat build/$*.ptxas.txt; exit 1)
 
 $(PKG)/libgc.so: $(GC_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(GC_OBJS) -lcudart -ldl
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(GC_OBJS) -ldl -lpthread -lrt
 
 clean:
 	rm -rf build gen/libgcgen.so oracle/liboracle.so $(PKG)/libgc.so

@@ -1,0 +1,324 @@
+// build_csr.cu — on-GPU graph construction.
+//
+//  a2  canonicalise: drop self loops, fold both orientations to (min, max),
+//      radix-sort the packed keys on 2b bits (b = id bits), unique
+//      (P:134-136 [Data Sets]: "all self loops were removed", "additional
+//      edges in the opposite direction were added"; reading A1: dedup).
+//  a3  degrees d(x) (Alg. 4 "d = sum(E)").
+//  a4  rank r(x) = position of (d(x), x) in lexicographic order; relabel
+//      every vertex by its rank and orient each edge low -> high rank.  In
+//      rank space the oriented graph is the strict upper triangle U of the
+//      relabelled A (Alg. 3's (L, U) <- A), whose rows are sorted and
+//      short: d+(x) <= sqrt(2m).  Also the transposed lists (in-lists) that
+//      the intersection kernels walk, grouped by head vertex.
+//
+// Radix sorts are CUB's (library primitive); everything else is ours.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "gc_internal.cuh"
+
+namespace gcx {
+
+namespace {
+
+__global__ void k_scan_ids(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz,
+                           int* __restrict__ maxid, int* __restrict__ neg) {
+    int mx = -1, ng = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        int a = __ldg(u + i), b = __ldg(v + i);
+        mx = max(mx, max(a, b));
+        ng |= (a < 0) | (b < 0);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    ng = __reduce_or_sync(0xffffffffu, (unsigned)ng);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(maxid, mx);
+        if (ng) atomicOr(neg, 1);
+    }
+}
+
+// key = (min << b) | max ; self loops -> sentinel (all ones in the low 2b bits,
+// never a real key since it would need min == max).
+__global__ void k_pack(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz, int b,
+                       uint64_t sent, uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
+        uint32_t lo = min(a, c), hi = max(a, c);
+        keys[i] = (a == c) ? sent : (((uint64_t)lo << b) | hi);
+    }
+}
+
+__global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ deg) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = canon[e];
+        atomicAdd(deg + (k >> b), 1);
+        atomicAdd(deg + (k & mask), 1);
+    }
+}
+
+__global__ void k_vkeys(const int32_t* __restrict__ deg, int64_t n, int b, uint64_t* __restrict__ keys) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        keys[x] = ((uint64_t)deg[x] << b) | (uint64_t)x;
+}
+
+__global__ void k_rank_scatter(const uint64_t* __restrict__ sorted, int64_t n, uint64_t mask,
+                               int32_t* __restrict__ rank_of) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        rank_of[sorted[r] & mask] = (int32_t)r;
+}
+
+// oriented key in rank space: (lo << b) | hi with lo = min rank, hi = max rank
+__global__ void k_orient(const uint64_t* __restrict__ canon, int64_t m, int b, const int32_t* __restrict__ rank_of,
+                         uint64_t* __restrict__ dkeys, int32_t* __restrict__ iota) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = canon[e];
+        uint32_t ra = (uint32_t)__ldg(rank_of + (k >> b)), rb = (uint32_t)__ldg(rank_of + (k & mask));
+        uint32_t lo = min(ra, rb), hi = max(ra, rb);
+        dkeys[e] = ((uint64_t)lo << b) | hi;
+        iota[e] = (int32_t)e;
+    }
+}
+
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, int64_t m, int b, int32_t* __restrict__ lo_out,
+                             int32_t* __restrict__ hi_out) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        hi_out[i] = (int32_t)(k >> b);   // row id (high part)
+        lo_out[i] = (int32_t)(k & mask); // column (low part)
+    }
+}
+
+// CSR row pointers from a row-sorted COO row array: ptr[x] = first i with row[i] >= x.
+__global__ void k_rows_from_sorted(const int32_t* __restrict__ row, int64_t m, int64_t n, int64_t* __restrict__ ptr) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prev = (i == 0) ? -1 : (int64_t)row[i - 1];
+        int64_t cur = (i == m) ? n : (int64_t)row[i];
+        for (int64_t x = prev + 1; x <= cur; ++x) ptr[x] = i;
+    }
+}
+
+__global__ void k_in_keys(const int32_t* __restrict__ col, const int32_t* __restrict__ src, int64_t m, int b,
+                          uint64_t* __restrict__ ikeys, int32_t* __restrict__ iota) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        ikeys[p] = ((uint64_t)(uint32_t)col[p] << b) | (uint32_t)src[p];
+        iota[p] = (int32_t)p;
+    }
+}
+
+// Work-model sums over vertices: wedges = Σ C(d+,2), Q_out = Σ d+², Q_in = Σ d- d+,
+// max d+, max d.
+__global__ void k_graph_stats(const int64_t* __restrict__ dag_ptr, const int64_t* __restrict__ in_ptr,
+                              const int32_t* __restrict__ deg, int64_t n, unsigned long long* __restrict__ acc) {
+    unsigned long long w = 0, qo = 0, qi = 0;
+    int mo = 0, md = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long dp = (unsigned long long)(dag_ptr[x + 1] - dag_ptr[x]);
+        unsigned long long dm = (unsigned long long)(in_ptr[x + 1] - in_ptr[x]);
+        w += dp * (dp - (dp > 0)) / 2;
+        qo += dp * dp;
+        qi += dm * dp;
+        mo = max(mo, (int)dp);
+        md = max(md, deg[x]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        w += __shfl_xor_sync(0xffffffffu, w, o);
+        qo += __shfl_xor_sync(0xffffffffu, qo, o);
+        qi += __shfl_xor_sync(0xffffffffu, qi, o);
+    }
+    mo = __reduce_max_sync(0xffffffffu, mo);
+    md = __reduce_max_sync(0xffffffffu, md);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(acc + 0, w);
+        atomicAdd(acc + 1, qo);
+        atomicAdd(acc + 2, qi);
+        atomicMax(acc + 3, (unsigned long long)mo);
+        atomicMax(acc + 4, (unsigned long long)md);
+    }
+}
+
+__global__ void k_unpack_canon(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ u,
+                               int32_t* __restrict__ v) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = canon[e];
+        u[e] = (int32_t)(k >> b);
+        v[e] = (int32_t)(k & mask);
+    }
+}
+
+}  // namespace
+
+// Sort keys (and optional int32 payload) on bits [0, nbits); results in
+// keys_out / vals_out.
+static int radix_sort(gc_ctx* c, const uint64_t* kin, uint64_t* kout, const int32_t* vin, int32_t* vout, int64_t N,
+                      int nbits) {
+    if (N <= 0) return GC_OK;
+    size_t tmp = 0;
+    if (vin) {
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, N, 0, nbits, c->stream));
+    } else {
+        GC_CUDA(c, cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, N, 0, nbits, c->stream));
+    }
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    if (vin) {
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, kin, kout, vin, vout, N, 0, nbits, c->stream));
+    } else {
+        GC_CUDA(c, cub::DeviceRadixSort::SortKeys(c->cub_tmp.p, tmp, kin, kout, N, 0, nbits, c->stream));
+    }
+    c->stats.lib_launches += 2 + (nbits + 7) / 8;   // histogram + scan + one onesweep pass per digit
+    return GC_OK;
+}
+
+int build_csr(gc_ctx* c) {
+    const int64_t nnz = c->nnz;
+    c->n = 0;
+    c->m = 0;
+    c->bits = 1;
+    GC_TRY(ensure(c, c->scal, 256));
+    int* d_scal = c->scal.as<int>();
+    GC_TRY(host_scratch(c, 4096));
+    int64_t* h = static_cast<int64_t*>(c->hpin);
+
+    // ---- n = max id + 1; reject negative ids
+    GC_CUDA(c, cudaMemsetAsync(d_scal, 0xff, sizeof(int), c->stream));       // maxid = -1
+    GC_CUDA(c, cudaMemsetAsync(d_scal + 1, 0, sizeof(int), c->stream));      // neg = 0
+    if (nnz > 0)
+        GC_LAUNCH(c, k_scan_ids, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
+                  d_scal, d_scal + 1);
+    GC_CUDA(c, cudaMemcpyAsync(h, d_scal, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    int maxid = reinterpret_cast<int*>(h)[0];
+    int neg = reinterpret_cast<int*>(h)[1];
+    if (neg) return fail(c, GC_ERR_INVALID, "gc_build_csr: negative vertex id");
+    if (maxid == INT32_MAX) return fail(c, GC_ERR_RANGE, "gc_build_csr: vertex id 2^31-1 leaves no room for n");
+    const int64_t n = (int64_t)maxid + 1;
+    c->n = n;
+    const int b = n > 1 ? ceil_log2_u64((uint64_t)n) : 1;
+    c->bits = b;
+    const uint64_t mask = (1ULL << b) - 1;
+
+    // ---- a2: pack, sort, unique
+    int64_t m = 0;
+    if (nnz > 0) {
+        GC_TRY(ensure(c, c->keys_a, (size_t)nnz * 8));
+        GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
+        const uint64_t sent = (2 * b >= 64) ? ~0ULL : ((1ULL << (2 * b)) - 1);
+        GC_LAUNCH(c, k_pack, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz, b, sent,
+                  c->keys_a.as<uint64_t>());
+        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nullptr, nullptr, nnz, 2 * b));
+        GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
+        int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
+        size_t tmp = 0;
+        GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(), d_nsel,
+                                             nnz, c->stream));
+        GC_TRY(ensure(c, c->cub_tmp, tmp));
+        tmp = c->cub_tmp.cap;
+        GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
+                                             d_nsel, nnz, c->stream));
+        c->stats.lib_launches += 2;
+        GC_CUDA(c, cudaMemcpyAsync(h, d_nsel, 8, cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(sync(c));
+        int64_t nsel = h[0];
+        if (nsel > 0) {
+            GC_CUDA(c, cudaMemcpyAsync(h + 1, c->canon.as<uint64_t>() + nsel - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+            GC_TRY(sync(c));
+            m = nsel - ((uint64_t)h[1] == sent ? 1 : 0);
+        }
+    }
+    if (m >= ((int64_t)1 << 31) - 1) return fail(c, GC_ERR_RANGE, "gc_build_csr: m >= 2^31 (edge ids are int32)");
+    c->m = m;
+
+    // ---- a3: degrees
+    GC_TRY(ensure(c, c->deg, (size_t)n * 4));
+    GC_TRY(ensure(c, c->rank_of, (size_t)n * 4));
+    GC_TRY(ensure(c, c->dag_ptr, (size_t)(n + 1) * 8));
+    GC_TRY(ensure(c, c->in_ptr, (size_t)(n + 1) * 8));
+    GC_TRY(ensure(c, c->dag_col, (size_t)m * 4));
+    GC_TRY(ensure(c, c->dag_src, (size_t)m * 4));
+    GC_TRY(ensure(c, c->dag_eid, (size_t)m * 4));
+    GC_TRY(ensure(c, c->in_pos, (size_t)m * 4));
+    GC_TRY(ensure(c, c->in_src, (size_t)m * 4));
+    GC_TRY(ensure(c, c->in_dst, (size_t)m * 4));
+    GC_TRY(ensure(c, c->vals_a, (size_t)(m > n ? m : n) * 4));
+    GC_TRY(ensure(c, c->vals_b, (size_t)(m > n ? m : n) * 4));
+    GC_TRY(ensure(c, c->keys_a, (size_t)(m > n ? m : n) * 8));
+    GC_TRY(ensure(c, c->keys_b, (size_t)(m > n ? m : n) * 8));
+    GC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)n * 4, c->stream));
+    if (m > 0)
+        GC_LAUNCH(c, k_degrees, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->deg.as<int32_t>());
+
+    // ---- a4: rank = sorted position of (deg, id); relabel + orient
+    if (n > 0) {
+        GC_LAUNCH(c, k_vkeys, grid_for(n), kThreads, 0, c->deg.as<int32_t>(), n, b, c->keys_a.as<uint64_t>());
+        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nullptr, nullptr, n, 2 * b));
+        GC_LAUNCH(c, k_rank_scatter, grid_for(n), kThreads, 0, c->keys_b.as<uint64_t>(), n, mask,
+                  c->rank_of.as<int32_t>());
+    }
+    if (m > 0) {
+        GC_LAUNCH(c, k_orient, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->rank_of.as<int32_t>(),
+                  c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
+        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
+                          c->dag_eid.as<int32_t>(), m, 2 * b));
+        GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->dag_col.as<int32_t>(),
+                  c->dag_src.as<int32_t>());
+    }
+    GC_LAUNCH(c, k_rows_from_sorted, grid_for(m + 1), kThreads, 0, c->dag_src.as<int32_t>(), m, n,
+              c->dag_ptr.as<int64_t>());
+    // in-lists: sort (head, tail) with the DAG position as payload
+    if (m > 0) {
+        GC_LAUNCH(c, k_in_keys, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), c->dag_src.as<int32_t>(), m, b,
+                  c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
+        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
+                          c->in_pos.as<int32_t>(), m, 2 * b));
+        GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->in_src.as<int32_t>(),
+                  c->in_dst.as<int32_t>());
+    }
+    GC_LAUNCH(c, k_rows_from_sorted, grid_for(m + 1), kThreads, 0, c->in_dst.as<int32_t>(), m, n,
+              c->in_ptr.as<int64_t>());
+
+    // ---- work-model statistics (one reduction over vertices)
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_scal + 16);
+    GC_CUDA(c, cudaMemsetAsync(acc, 0, 5 * 8, c->stream));
+    if (n > 0)
+        GC_LAUNCH(c, k_graph_stats, grid_for(n), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(),
+                  c->deg.as<int32_t>(), n, acc);
+    GC_CUDA(c, cudaMemcpyAsync(h, acc, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    c->stats.n = n;
+    c->stats.m = m;
+    c->stats.wedges = h[0];
+    c->stats.q_out = h[1];
+    c->stats.q_in = h[2];
+    c->stats.max_out_degree = h[3];
+    c->stats.max_degree = h[4];
+    return GC_OK;
+}
+
+int get_edges(gc_ctx* c, int32_t* u_out, int32_t* v_out) {
+    const int64_t m = c->m;
+    if (m == 0) return GC_OK;
+    GC_TRY(ensure(c, c->vals_a, (size_t)m * 4));
+    GC_TRY(ensure(c, c->vals_b, (size_t)m * 4));
+    GC_LAUNCH(c, k_unpack_canon, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, c->bits,
+              c->vals_a.as<int32_t>(), c->vals_b.as<int32_t>());
+    GC_TRY(copy_out(c, u_out, c->vals_a.p, (size_t)m * 4));
+    GC_TRY(copy_out(c, v_out, c->vals_b.p, (size_t)m * 4));
+    GC_TRY(sync(c));
+    return GC_OK;
+}
+
+}  // namespace gcx
+
+extern "C" int gc_get_edges(gc_ctx* c, int32_t* u_out, int32_t* v_out) {
+    if (!c) return GC_ERR_INVALID;
+    if (c->poisoned) return GC_ERR_STATE;
+    if (c->state < 2) return gcx::fail(c, GC_ERR_STATE, "gc_get_edges before gc_build_csr");
+    if (c->m > 0 && (!u_out || !v_out)) return gcx::fail(c, GC_ERR_INVALID, "gc_get_edges: NULL output");
+    cudaSetDevice(c->device);
+    return gcx::get_edges(c, u_out, v_out);
+}

@@ -1,0 +1,128 @@
+// comm.cu — NCCL over NVLink for the multi-GPU path.
+//
+// libnccl.so.2 is resolved with dlopen at gc_comm_init time, so libgc loads
+// (and runs single-GPU) without NCCL, and inside a PyTorch process it reuses
+// the NCCL that torch already loaded (same soname).  Collectives run on the
+// context stream:
+//   triangle count  ncclAllReduce(uint64, sum, 1)
+//   edge support    ncclAllReduce(uint32, sum, m)
+//   k-truss peel    ncclAllGather of the removed-edge bitmap (per round)
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "gc_internal.cuh"
+
+namespace gcx {
+
+namespace {
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+NcclApi& api() {
+    static NcclApi A;
+    static bool tried = false;
+    if (tried) return A;
+    tried = true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+        A.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+        if (A.h) break;
+    }
+    if (!A.h) {
+        A.why = std::string("dlopen(libnccl.so.2) failed: ") + (dlerror() ? dlerror() : "?");
+        return A;
+    }
+#define SYM(field, name)                                                   \
+    A.field = reinterpret_cast<decltype(A.field)>(dlsym(A.h, name));       \
+    if (!A.field) {                                                        \
+        A.why = std::string("NCCL symbol missing: ") + name;               \
+        return A;                                                          \
+    }
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(CommAbort, "ncclCommAbort");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(AllGather, "ncclAllGather");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    A.ok = true;
+    return A;
+}
+
+int nccl_fail(gc_ctx* c, ncclResult_t r, const char* what) {
+    std::string msg = std::string("NCCL error in ") + what + ": " +
+                      (api().GetErrorString ? api().GetErrorString(r) : "?");
+    if (c) {
+        c->poisoned = true;
+        if (c->nccl && api().CommAbort) {
+            api().CommAbort(static_cast<ncclComm_t>(c->nccl));
+            c->nccl = nullptr;
+        }
+    }
+    return fail(c, GC_ERR_NCCL, msg);
+}
+
+}  // namespace
+
+int nccl_get_unique_id(void* id) {
+    NcclApi& A = api();
+    if (!A.ok) return GC_ERR_NCCL;
+    ncclUniqueId uid;
+    if (A.GetUniqueId(&uid) != ncclSuccess) return GC_ERR_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id, &uid, sizeof(uid));
+    return GC_OK;
+}
+
+int nccl_init(gc_ctx* c, const void* id, int nranks, int rank) {
+    NcclApi& A = api();
+    if (!A.ok) return fail(c, GC_ERR_NCCL, A.why);
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm = nullptr;
+    ncclResult_t r = A.CommInitRank(&comm, nranks, uid, rank);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclCommInitRank");
+    c->nccl = comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    return GC_OK;
+}
+
+int nccl_destroy(gc_ctx* c) {
+    if (c->nccl && api().ok) api().CommDestroy(static_cast<ncclComm_t>(c->nccl));
+    c->nccl = nullptr;
+    return GC_OK;
+}
+
+int allreduce_u64(gc_ctx* c, uint64_t* dev, size_t count) {
+    ncclResult_t r = api().AllReduce(dev, dev, count, ncclUint64, ncclSum, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllReduce(u64)");
+    return GC_OK;
+}
+
+int allreduce_u32(gc_ctx* c, uint32_t* dev, size_t count) {
+    ncclResult_t r = api().AllReduce(dev, dev, count, ncclUint32, ncclSum, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllReduce(u32)");
+    return GC_OK;
+}
+
+int allgather_u32(gc_ctx* c, const uint32_t* send, uint32_t* recv, size_t count_per_rank) {
+    ncclResult_t r = api().AllGather(send, recv, count_per_rank, ncclUint32, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllGather(u32)");
+    return GC_OK;
+}
+
+}  // namespace gcx

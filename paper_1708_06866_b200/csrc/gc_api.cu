@@ -1,0 +1,363 @@
+// gc_api.cu — the extern "C" entry points of include/gc.h and the context
+// plumbing (errors, stream-ordered buffers, host<->device copies).
+#include <cstring>
+#include <new>
+
+#include "gc_internal.cuh"
+
+namespace gcx {
+
+int fail(gc_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(gc_ctx* c, cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+             cudaGetErrorString(e), what, file, line);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear the sticky-free allocation error
+        return fail(c, GC_ERR_OOM, buf);
+    }
+    if (c) c->poisoned = true;
+    return fail(c, GC_ERR_CUDA, buf);
+}
+
+int ensure(gc_ctx* c, Buf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return GC_OK;
+    if (b.p) {
+        GC_CUDA(c, cudaFreeAsync(b.p, c->stream));
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t want = bytes + bytes / 8;  // slack so growing configs do not thrash
+    cudaError_t e = cudaMallocAsync(&b.p, want, c->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        // retry without slack
+        e = cudaMallocAsync(&b.p, bytes, c->stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            char msg[128];
+            snprintf(msg, sizeof(msg), "device allocation of %zu bytes failed", bytes);
+            return fail(c, GC_ERR_OOM, msg);
+        }
+        want = bytes;
+    }
+    b.cap = want;
+    return GC_OK;
+}
+
+void release(gc_ctx* c, Buf& b) {
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+int host_scratch(gc_ctx* c, size_t bytes) {
+    if (c->hpin_cap >= bytes) return GC_OK;
+    if (c->hpin) cudaFreeHost(c->hpin);
+    c->hpin = nullptr;
+    c->hpin_cap = 0;
+    GC_CUDA(c, cudaMallocHost(&c->hpin, bytes));
+    c->hpin_cap = bytes;
+    return GC_OK;
+}
+
+int sync(gc_ctx* c) {
+    GC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return GC_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int copy_out(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes) {
+    if (nbytes == 0) return GC_OK;
+    cudaMemcpyKind kind = is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    GC_CUDA(c, cudaMemcpyAsync(dst, src_dev, nbytes, kind, c->stream));
+    return GC_OK;
+}
+
+int copy_in(gc_ctx* c, void* dst_dev, const void* src, size_t nbytes) {
+    if (nbytes == 0) return GC_OK;
+    cudaMemcpyKind kind = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    GC_CUDA(c, cudaMemcpyAsync(dst_dev, src, nbytes, kind, c->stream));
+    return GC_OK;
+}
+
+int record(gc_ctx* c, int i) {
+    if (!c->timing) return GC_OK;
+    GC_CUDA(c, cudaEventRecord(c->ev[i], c->stream));
+    return GC_OK;
+}
+
+float elapsed(gc_ctx* c, int a, int b) {
+    if (!c->timing) return 0.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+}  // namespace gcx
+
+using namespace gcx;
+
+static int check_ctx(const gc_ctx* c) {
+    if (!c) return GC_ERR_INVALID;
+    if (c->poisoned) return GC_ERR_STATE;
+    return GC_OK;
+}
+
+static thread_local std::string g_create_err;
+
+extern "C" {
+
+int gc_create(gc_ctx** out, int device, void* cuda_stream) {
+    if (!out) return GC_ERR_INVALID;
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        g_create_err = std::string("gc_create: no CUDA device ") + std::to_string(device) +
+                       (e != cudaSuccess ? std::string(" (") + cudaGetErrorString(e) + ")" : "");
+        return e != cudaSuccess ? GC_ERR_CUDA : GC_ERR_INVALID;
+    }
+    gc_ctx* c = new (std::nothrow) gc_ctx();
+    if (!c) return GC_ERR_OOM;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        g_create_err = "gc_create: cudaSetDevice failed";
+        delete c;
+        return GC_ERR_CUDA;
+    }
+    if (cuda_stream) {
+        c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            g_create_err = "gc_create: cudaStreamCreate failed";
+            delete c;
+            return GC_ERR_CUDA;
+        }
+        c->own_stream = true;
+    }
+    // keep freed pool memory cached: steady-state steps then allocate nothing
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    for (auto& ev : c->ev) cudaEventCreate(&ev);
+    cudaGetLastError();
+    *out = c;
+    return GC_OK;
+}
+
+int gc_destroy(gc_ctx* c) {
+    if (!c) return GC_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
+                        &c->dag_col, &c->dag_src, &c->dag_eid, &c->in_ptr, &c->in_pos, &c->in_src,
+                        &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
+                        &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp,
+                        &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->rem, &c->front_a,
+                        &c->front_b, &c->tau, &c->bitmap};
+    for (auto* b : bufs) release(c, *b);
+    cudaStreamSynchronize(c->stream);
+    nccl_destroy(c);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    for (auto& ev : c->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    cudaGetLastError();
+    delete c;
+    return GC_OK;
+}
+
+const char* gc_last_error(const gc_ctx* c) {
+    if (!c) return g_create_err.c_str();
+    return c->err.c_str();
+}
+
+int gc_nccl_unique_id(void* id_out) {
+    if (!id_out) return GC_ERR_INVALID;
+    return nccl_get_unique_id(id_out);
+}
+
+int gc_comm_init(gc_ctx* c, const void* id, int nranks, int rank) {
+    GC_TRY(check_ctx(c));
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, GC_ERR_INVALID, "gc_comm_init: bad arguments");
+    if (c->state != 0) return fail(c, GC_ERR_STATE, "gc_comm_init must precede gc_load_edges");
+    if (c->nccl || c->loop_parts) return fail(c, GC_ERR_STATE, "communicator already initialised");
+    cudaSetDevice(c->device);
+    if (nranks == 1) {
+        c->nranks = 1;
+        c->rank = 0;
+        return GC_OK;
+    }
+    return nccl_init(c, id, nranks, rank);
+}
+
+int gc_comm_init_loopback(gc_ctx* c, int nparts) {
+    GC_TRY(check_ctx(c));
+    if (nparts < 1 || nparts > 64) return fail(c, GC_ERR_INVALID, "gc_comm_init_loopback: nparts must be 1..64");
+    if (c->state != 0) return fail(c, GC_ERR_STATE, "gc_comm_init_loopback must precede gc_load_edges");
+    if (c->nccl) return fail(c, GC_ERR_STATE, "communicator already initialised");
+    c->loop_parts = nparts;
+    c->nranks = 1;
+    c->rank = 0;
+    return GC_OK;
+}
+
+int gc_load_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
+    GC_TRY(check_ctx(c));
+    if (nnz < 0 || (nnz > 0 && (!u || !v))) return fail(c, GC_ERR_INVALID, "gc_load_edges: bad arguments");
+    cudaSetDevice(c->device);
+    GC_TRY(ensure(c, c->raw_u, (size_t)nnz * sizeof(int32_t)));
+    GC_TRY(ensure(c, c->raw_v, (size_t)nnz * sizeof(int32_t)));
+    GC_TRY(copy_in(c, c->raw_u.p, u, (size_t)nnz * sizeof(int32_t)));
+    GC_TRY(copy_in(c, c->raw_v.p, v, (size_t)nnz * sizeof(int32_t)));
+    GC_TRY(sync(c));
+    c->nnz = nnz;
+    c->state = 1;
+    c->tasks_ready = false;
+    c->sym_ready = false;
+    c->n = c->m = 0;
+    return GC_OK;
+}
+
+int gc_build_csr(gc_ctx* c) {
+    GC_TRY(check_ctx(c));
+    if (c->state < 1) return fail(c, GC_ERR_STATE, "gc_build_csr before gc_load_edges");
+    cudaSetDevice(c->device);
+    c->state = 1;
+    c->tasks_ready = false;
+    c->sym_ready = false;
+    GC_TRY(record(c, 0));
+    GC_TRY(build_csr(c));
+    GC_TRY(prepare_tasks(c));
+    GC_TRY(record(c, 1));
+    GC_TRY(sync(c));
+    c->stats.build_ms = elapsed(c, 0, 1);
+    c->state = 2;
+    return GC_OK;
+}
+
+int gc_num_vertices(const gc_ctx* c, int64_t* n) {
+    GC_TRY(check_ctx(c));
+    if (!n) return GC_ERR_INVALID;
+    if (c->state < 2) return GC_ERR_STATE;
+    *n = c->n;
+    return GC_OK;
+}
+
+int gc_num_edges(const gc_ctx* c, int64_t* m) {
+    GC_TRY(check_ctx(c));
+    if (!m) return GC_ERR_INVALID;
+    if (c->state < 2) return GC_ERR_STATE;
+    *m = c->m;
+    return GC_OK;
+}
+
+int gc_triangle_count(gc_ctx* c, uint64_t* count) {
+    GC_TRY(check_ctx(c));
+    if (!count) return fail(c, GC_ERR_INVALID, "gc_triangle_count: NULL output");
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_triangle_count before gc_build_csr");
+    cudaSetDevice(c->device);
+    return triangle_count(c, count);
+}
+
+int gc_edge_support(gc_ctx* c, uint32_t* support_out) {
+    GC_TRY(check_ctx(c));
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_edge_support before gc_build_csr");
+    if (!support_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_edge_support: NULL output");
+    cudaSetDevice(c->device);
+    GC_TRY(record(c, 4));
+    GC_TRY(support_dag(c));
+    GC_TRY(ensure(c, c->out_tmp, (size_t)c->m * sizeof(uint32_t)));
+    GC_TRY(scatter_canonical_u32(c, c->sup.as<uint32_t>(), c->out_tmp.as<uint32_t>()));
+    GC_TRY(record(c, 5));
+    GC_TRY(copy_out(c, support_out, c->out_tmp.p, (size_t)c->m * sizeof(uint32_t)));
+    GC_TRY(sync(c));
+    c->stats.support_ms = elapsed(c, 4, 5);
+    c->stats.support_kernel_ms = elapsed(c, 6, 7);
+    return GC_OK;
+}
+
+int gc_ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
+    GC_TRY(check_ctx(c));
+    if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss: k must be >= 2 (P:280)");
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss before gc_build_csr");
+    if (!alive_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_ktruss: NULL output");
+    cudaSetDevice(c->device);
+    return ktruss(c, k, alive_out, m_alive);
+}
+
+int gc_truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
+    GC_TRY(check_ctx(c));
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_truss_decomposition before gc_build_csr");
+    if (!kmax || (!tau_out && c->m > 0)) return fail(c, GC_ERR_INVALID, "gc_truss_decomposition: NULL output");
+    cudaSetDevice(c->device);
+    return truss_decomposition(c, tau_out, kmax);
+}
+
+int gc_set_option(gc_ctx* c, int option, int64_t value) {
+    GC_TRY(check_ctx(c));
+    switch (option) {
+        case GC_OPT_FORCE_CLASS:
+            if (value < -1 || value > 3) return fail(c, GC_ERR_INVALID, "force class must be -1..3");
+            c->force_class = (int)value;
+            c->tasks_ready = false;
+            if (c->state == 2) {
+                cudaSetDevice(c->device);
+                GC_TRY(prepare_tasks(c));
+                GC_TRY(sync(c));
+            }
+            return GC_OK;
+        case GC_OPT_TASK_CHUNK:
+            if (value < 32 || value > (int64_t)1 << 30) return fail(c, GC_ERR_INVALID, "task chunk out of range");
+            c->task_chunk = value;
+            c->tasks_ready = false;
+            if (c->state == 2) {
+                cudaSetDevice(c->device);
+                GC_TRY(prepare_tasks(c));
+                GC_TRY(sync(c));
+            }
+            return GC_OK;
+        case GC_OPT_TIMING:
+            c->timing = value ? 1 : 0;
+            return GC_OK;
+        default:
+            return fail(c, GC_ERR_INVALID, "unknown option");
+    }
+}
+
+int gc_get_stats(const gc_ctx* c, gc_stats* out) {
+    if (!c || !out) return GC_ERR_INVALID;
+    *out = c->stats;
+    return GC_OK;
+}
+
+int gc_reset_stats(gc_ctx* c) {
+    if (!c) return GC_ERR_INVALID;
+    c->stats.launches = 0;
+    c->stats.lib_launches = 0;
+    return GC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// gc_internal.cuh — libgc internals: context, device buffers, error plumbing.
+//
+// Layout in HBM: every graph array lives in one
+// gc_ctx and is reused across calls (grow-only, stream-ordered allocations
+// from the CUDA memory pool), so a steady-state step allocates nothing.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "gc.h"
+
+namespace gcx {
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Status plumbing ------------------------------------------------------------
+#define GC_TRY(expr)                         \
+    do {                                     \
+        int _rc = (expr);                    \
+        if (_rc != GC_OK) return _rc;        \
+    } while (0)
+
+#define GC_CUDA(ctx, expr)                                                         \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) return gcx::cuda_fail((ctx), _e, #expr, __FILE__, __LINE__); \
+    } while (0)
+
+// Every libgc kernel launch goes through this macro: it counts the launch
+// (gc_stats.launches, the bench's "gpu_launches") and checks the launch.
+#define GC_LAUNCH(ctx, kernel, grid, block, smem, ...)                                  \
+    do {                                                                                \
+        (ctx)->stats.launches++;                                                        \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                \
+        cudaError_t _e = cudaGetLastError();                                            \
+        if (_e != cudaSuccess) return gcx::cuda_fail((ctx), _e, #kernel, __FILE__, __LINE__); \
+    } while (0)
+
+}  // namespace gcx
+
+struct gc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    bool poisoned = false;
+    int state = 0;  // 0 created, 1 edges loaded, 2 graph built
+
+    // options
+    int force_class = -1;
+    int64_t task_chunk = 4096;
+    int timing = 1;
+
+    // raw input (a1)
+    gcx::Buf raw_u, raw_v;
+    int64_t nnz = 0;
+
+    // graph sizes
+    int64_t n = 0, m = 0;
+    int bits = 1;  // b: vertex id bits; keys pack (hi << b) | lo
+
+    // canonical list (a2): uint64 key (min << b) | max, m entries
+    gcx::Buf canon;
+    // degrees (a3), rank relabelling (a4)
+    gcx::Buf deg;       // int32[n]
+    gcx::Buf rank_of;   // int32[n] old id -> rank (new id)
+    // oriented DAG in rank space (a4): row x = N+(x) ascending
+    gcx::Buf dag_ptr;   // int64[n+1]
+    gcx::Buf dag_col;   // int32[m]
+    gcx::Buf dag_src;   // int32[m]
+    gcx::Buf dag_eid;   // int32[m] canonical edge id of DAG position p
+    // in-lists grouped by head v, ascending tail u (a4/a5)
+    gcx::Buf in_ptr;    // int64[n+1]
+    gcx::Buf in_pos;    // int32[m]  DAG position p of edge u->v
+    gcx::Buf in_src;    // int32[m]  u
+    gcx::Buf in_dst;    // int32[m]  v (head; in-list is sorted by (v, u))
+    // intersection tasks (a5)
+    gcx::Buf task_i0;   // int32 first in-list index of each task (tasks grouped by class)
+    gcx::Buf task_i1;   // int32 one past the last in-list index of each task
+    gcx::Buf in_cost;   // int64[m] exclusive cost prefix over the in-list
+    gcx::Buf tmp_a, tmp_b;  // task construction scratch
+    int64_t ntask[4] = {0, 0, 0, 0};
+    int64_t task_off[5] = {0, 0, 0, 0, 0};
+    int64_t total_cost = 0;
+    int task_parts = 1;     // number of owners the tasks were cut for
+    bool tasks_ready = false;
+
+    // scratch
+    gcx::Buf keys_a, keys_b;    // uint64 sort buffers
+    gcx::Buf vals_a, vals_b;    // int32 sort payloads
+    gcx::Buf cub_tmp;
+    gcx::Buf scal;              // small device scalars (counters, reductions)
+    gcx::Buf sup;               // uint32[m] support in DAG-position order
+    gcx::Buf out_tmp;           // staging for canonical-order outputs
+
+    // peeler (a8/a9)
+    gcx::Buf sym_ptr;   // int64[n+1]
+    gcx::Buf sym_col;   // int32[2m]
+    gcx::Buf sym_eid;   // int32[2m] DAG position of the edge
+    bool sym_ready = false;
+    gcx::Buf alive;     // uint8[m]
+    gcx::Buf rem;       // int32[m] round in which the edge is in the frontier
+    gcx::Buf front_a, front_b;  // int32[m] frontier lists
+    gcx::Buf tau;       // int32[m]
+    gcx::Buf bitmap;    // uint32 removed-edge bitmap (multi-GPU exchange)
+
+    // pinned host scratch
+    void* hpin = nullptr;
+    size_t hpin_cap = 0;
+
+    // events
+    cudaEvent_t ev[8] = {};
+
+    gc_stats stats = {};
+
+    // multi-GPU
+    int nranks = 1, rank = 0;
+    int loop_parts = 0;       // > 0: loopback virtual ranks on this GPU
+    void* nccl = nullptr;     // ncclComm_t
+};
+
+namespace gcx {
+
+int cuda_fail(gc_ctx* c, cudaError_t e, const char* what, const char* file, int line);
+int fail(gc_ctx* c, int code, const std::string& msg);
+int ensure(gc_ctx* c, Buf& b, size_t bytes);
+void release(gc_ctx* c, Buf& b);
+int host_scratch(gc_ctx* c, size_t bytes);
+int sync(gc_ctx* c);
+// copy nbytes from device src to a caller pointer (host or device)
+int copy_out(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes);
+int copy_in(gc_ctx* c, void* dst_dev, const void* src, size_t nbytes);
+float elapsed(gc_ctx* c, int a, int b);
+int record(gc_ctx* c, int i);
+
+// build_csr.cu
+int build_csr(gc_ctx* c);
+// tc.cu
+int prepare_tasks(gc_ctx* c);
+int triangle_count(gc_ctx* c, uint64_t* out);
+int support_dag(gc_ctx* c);   // fills c->sup (DAG order), all ranks combined
+int scatter_canonical_u32(gc_ctx* c, const uint32_t* dag_vals, uint32_t* canon_out_dev);
+// peel.cu
+int build_sym(gc_ctx* c);
+int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive);
+int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax);
+// comm.cu
+int nccl_get_unique_id(void* id);
+int nccl_init(gc_ctx* c, const void* id, int nranks, int rank);
+int nccl_destroy(gc_ctx* c);
+int allreduce_u64(gc_ctx* c, uint64_t* dev, size_t count);
+int allreduce_u32(gc_ctx* c, uint32_t* dev, size_t count);
+int allgather_u32(gc_ctx* c, const uint32_t* send, uint32_t* recv, size_t count_per_rank);
+
+inline int ceil_log2_u64(uint64_t x) {  // bits needed to represent values < x (x >= 1)
+    int b = 0;
+    while ((1ULL << b) < x) ++b;
+    return b;
+}
+
+constexpr int kThreads = 256;
+inline int grid_for(int64_t n, int threads = kThreads, int cap = 148 * 16) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+}  // namespace gcx

@@ -1,0 +1,286 @@
+// peel.cu — incremental k-truss peeler and truss decomposition (SURVEY
+// §8(a) rows a8, a9).
+//
+// Method: P:247 [k-Truss] "each edge is contained in at least (k-2)
+// triangles in the same subgraph"; Alg. 4 removes, per round,
+// the whole vector x = find(s < k-2) and updates R = EA by subtracting the
+// removed edges' contribution instead of recomputing it.  The
+// element-wise meaning of that update: every triangle alive at the start of
+// the round that loses at least one edge costs each of its surviving edges
+// exactly one unit of support.  On the GPU:
+//
+//   frontier X (edges with s < k-2, alive)                   -- Alg. 4 "x"
+//   one warp per e in X: enumerate the live triangles through e by searching
+//     the shorter endpoint row in the longer one (symmetric CSR, rank space);
+//     a triangle with several edges in X is handled only by its smallest-id
+//     edge in X (reading A5), which decrements each survivor once
+//     (atomicSub); a survivor crossing from k-2 to k-3 joins the next
+//     frontier (threshold crossing: no full rescan per round)
+//   alive -= X
+//
+// until X is empty (fixed point).  Decomposition: k = 3, 4, ...
+// continue from the previous k's survivors; edges removed at level k get
+// trussness k-1.
+#include "gc_internal.cuh"
+
+namespace gcx {
+
+namespace {
+
+__global__ void k_sym_fill(const int32_t* __restrict__ in_src, const int32_t* __restrict__ in_dst,
+                           const int32_t* __restrict__ in_pos, const int32_t* __restrict__ dag_src,
+                           const int32_t* __restrict__ dag_col, const int64_t* __restrict__ dag_ptr,
+                           const int64_t* __restrict__ in_ptr, int64_t m, int32_t* __restrict__ col,
+                           int32_t* __restrict__ eid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        // lower part of row x = in_dst[i]: slot dag_ptr[x] + i
+        int x = in_dst[i];
+        int64_t s = dag_ptr[x] + i;
+        col[s] = in_src[i];
+        eid[s] = in_pos[i];
+        // upper part of row y = dag_src[i] (DAG position i): slot in_ptr[y+1] + i
+        int y = dag_src[i];
+        int64_t t = in_ptr[y + 1] + i;
+        col[t] = dag_col[i];
+        eid[t] = (int32_t)i;
+    }
+}
+
+__global__ void k_sym_ptr(const int64_t* __restrict__ dag_ptr, const int64_t* __restrict__ in_ptr, int64_t n,
+                          int64_t* __restrict__ sym_ptr) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n; x += (int64_t)gridDim.x * blockDim.x)
+        sym_ptr[x] = dag_ptr[x] + in_ptr[x];
+}
+
+__global__ void k_fill_u8(uint8_t* __restrict__ a, int64_t m, uint8_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ a, int64_t m, int32_t v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+
+// X = {alive e : S(e) < thr}
+__global__ void k_frontier_scan(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive, int64_t m,
+                                uint32_t thr, int32_t* __restrict__ rem, int32_t round, int32_t* __restrict__ front,
+                                int* __restrict__ count) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        bool in = alive[e] && S[e] < thr;
+        unsigned ballot = __ballot_sync(__activemask(), in);
+        if (in) {
+            rem[e] = round;
+            // warp-aggregated append
+            int leader = __ffs(ballot) - 1;
+            int lane = threadIdx.x & 31;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(count, __popc(ballot));
+            base = __shfl_sync(ballot, base, leader);
+            front[base + __popc(ballot & ((1u << lane) - 1))] = (int32_t)e;
+        }
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t lo, int64_t hi, int32_t x) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// One warp per frontier edge e = (a, b): destroy its live triangles.
+__global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front, int nfront,
+                                              const int32_t* __restrict__ dag_src, const int32_t* __restrict__ dag_col,
+                                              const int64_t* __restrict__ sym_ptr, const int32_t* __restrict__ sym_col,
+                                              const int32_t* __restrict__ sym_eid, const uint8_t* __restrict__ alive,
+                                              int32_t* __restrict__ rem, uint32_t* __restrict__ S, uint32_t thr,
+                                              int32_t round, int32_t* __restrict__ next, int* __restrict__ next_count) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
+        const int e = front[wi];
+        const int a = dag_src[e], b = dag_col[e];
+        int64_t a0 = sym_ptr[a], a1 = sym_ptr[a + 1], b0 = sym_ptr[b], b1 = sym_ptr[b + 1];
+        // iterate the shorter row, search the longer
+        if (a1 - a0 > b1 - b0) {
+            int64_t t0 = a0, t1 = a1;
+            a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+        }
+        for (int64_t i = a0 + lane; i < a1; i += 32) {
+            const int f = __ldg(sym_eid + i);
+            if (f == e || !alive[f]) continue;
+            const int32_t w = __ldg(sym_col + i);
+            const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
+            if (j >= b1 || __ldg(sym_col + j) != w) continue;
+            const int g = __ldg(sym_eid + j);
+            if (!alive[g]) continue;
+            const bool fx = rem[f] == round, gx = rem[g] == round;
+            if ((fx && f < e) || (gx && g < e)) continue;   // a smaller X-edge owns this triangle
+            if (!fx) {
+                uint32_t old = atomicSub(S + f, 1u);
+                if (old == thr) {
+                    rem[f] = round + 1;
+                    next[atomicAdd(next_count, 1)] = f;
+                }
+            }
+            if (!gx) {
+                uint32_t old = atomicSub(S + g, 1u);
+                if (old == thr) {
+                    rem[g] = round + 1;
+                    next[atomicAdd(next_count, 1)] = g;
+                }
+            }
+        }
+    }
+}
+
+__global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, uint8_t* __restrict__ alive,
+                               int32_t* __restrict__ tau, int32_t level) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
+        int e = front[i];
+        alive[e] = 0;
+        if (tau) tau[e] = level;
+    }
+}
+
+__global__ void k_scatter_u8(const uint8_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
+                             uint8_t* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
+        out[eid[p]] = vals[p];
+}
+
+__global__ void k_scatter_i32(const int32_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
+                              int32_t* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
+        out[eid[p]] = vals[p];
+}
+
+}  // namespace
+
+int build_sym(gc_ctx* c) {
+    if (c->sym_ready) return GC_OK;
+    const int64_t n = c->n, m = c->m;
+    GC_TRY(ensure(c, c->sym_ptr, (size_t)(n + 1) * 8));
+    GC_TRY(ensure(c, c->sym_col, (size_t)2 * m * 4));
+    GC_TRY(ensure(c, c->sym_eid, (size_t)2 * m * 4));
+    GC_LAUNCH(c, k_sym_ptr, grid_for(n + 1), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(), n,
+              c->sym_ptr.as<int64_t>());
+    if (m > 0)
+        GC_LAUNCH(c, k_sym_fill, grid_for(m), kThreads, 0, c->in_src.as<int32_t>(), c->in_dst.as<int32_t>(),
+                  c->in_pos.as<int32_t>(), c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                  c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(), m, c->sym_col.as<int32_t>(),
+                  c->sym_eid.as<int32_t>());
+    c->sym_ready = true;
+    return GC_OK;
+}
+
+// Peel at threshold thr = k - 2 starting from the current alive set / S.
+// level >= 0: write tau = level for removed edges.  Returns removed count.
+static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed) {
+    const int64_t m = c->m;
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
+    int32_t* h = static_cast<int32_t*>(c->hpin);
+    *removed = 0;
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
+    GC_LAUNCH(c, k_frontier_scan, grid_for(m), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), m, thr,
+              c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt);
+    GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    int nf = h[0];
+    int32_t* cur = c->front_a.as<int32_t>();
+    int32_t* nxt = c->front_b.as<int32_t>();
+    int* ncnt = cnt + 1;
+    while (nf > 0) {
+        GC_CUDA(c, cudaMemsetAsync(ncnt, 0, sizeof(int), c->stream));
+        const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
+        GC_LAUNCH(c, k_peel, blocks, 256, 0, cur, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                  c->sym_ptr.as<int64_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
+                  c->alive.as<uint8_t>(), c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, nxt, ncnt);
+        GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, cur, nf, c->alive.as<uint8_t>(),
+                  level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
+        GC_CUDA(c, cudaMemcpyAsync(h, ncnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(sync(c));
+        *removed += nf;
+        ++*round;
+        c->stats.peel_rounds++;
+        nf = h[0];
+        int32_t* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    ++*round;   // fresh stamp for the next level's scan
+    return GC_OK;
+}
+
+static int peel_setup(gc_ctx* c) {
+    const int64_t m = c->m;
+    GC_TRY(build_sym(c));
+    GC_TRY(ensure(c, c->alive, (size_t)m));
+    GC_TRY(ensure(c, c->rem, (size_t)m * 4));
+    GC_TRY(ensure(c, c->front_a, (size_t)m * 4));
+    GC_TRY(ensure(c, c->front_b, (size_t)m * 4));
+    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(host_scratch(c, 4096));
+    if (m > 0) {
+        GC_LAUNCH(c, k_fill_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, (uint8_t)1);
+        GC_LAUNCH(c, k_fill_i32, grid_for(m), kThreads, 0, c->rem.as<int32_t>(), m, (int32_t)-1);
+    }
+    c->stats.peel_rounds = 0;
+    return GC_OK;
+}
+
+int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
+    const int64_t m = c->m;
+    GC_TRY(record(c, 0));
+    GC_TRY(support_dag(c));                 // cold: support computed inside every call
+    GC_TRY(record(c, 2));
+    GC_TRY(peel_setup(c));
+    int64_t removed = 0;
+    if (m > 0 && k > 2) {
+        int32_t round = 0;
+        GC_TRY(peel_level(c, (uint32_t)(k - 2), -1, &round, &removed));
+    }
+    GC_TRY(ensure(c, c->out_tmp, (size_t)m));
+    if (m > 0)
+        GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(), m,
+                  c->out_tmp.as<uint8_t>());
+    GC_TRY(record(c, 1));
+    GC_TRY(copy_out(c, alive_out, c->out_tmp.p, (size_t)m));
+    GC_TRY(sync(c));
+    if (m_alive) *m_alive = m - removed;
+    c->stats.ktruss_ms = elapsed(c, 0, 1);
+    c->stats.peel_ms = elapsed(c, 2, 1);
+    return GC_OK;
+}
+
+int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
+    const int64_t m = c->m;
+    GC_TRY(record(c, 0));
+    GC_TRY(support_dag(c));
+    GC_TRY(record(c, 2));
+    GC_TRY(peel_setup(c));
+    GC_TRY(ensure(c, c->tau, (size_t)m * 4));
+    if (m > 0) GC_LAUNCH(c, k_fill_i32, grid_for(m), kThreads, 0, c->tau.as<int32_t>(), m, (int32_t)2);
+    int64_t left = m;
+    int32_t last = 0;
+    int32_t round = 0;
+    for (int32_t k = 3; left > 0; ++k) {
+        int64_t removed = 0;
+        GC_TRY(peel_level(c, (uint32_t)(k - 2), k - 1, &round, &removed));
+        if (removed > 0) last = k - 1;
+        left -= removed;
+    }
+    *kmax = (m > 0) ? last : 0;
+    GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
+    if (m > 0)
+        GC_LAUNCH(c, k_scatter_i32, grid_for(m), kThreads, 0, c->tau.as<int32_t>(), c->dag_eid.as<int32_t>(), m,
+                  c->out_tmp.as<int32_t>());
+    GC_TRY(record(c, 1));
+    GC_TRY(copy_out(c, tau_out, c->out_tmp.p, (size_t)m * 4));
+    GC_TRY(sync(c));
+    c->stats.decomp_ms = elapsed(c, 0, 1);
+    c->stats.peel_ms = elapsed(c, 2, 1);
+    return GC_OK;
+}
+
+}  // namespace gcx

@@ -1,0 +1,578 @@
+// tc.cu — per-edge triangle support and triangle count (SURVEY §8(a) rows
+// a5-a7): work estimate + task binning, and the sm_100a intersection kernels.
+//
+// Method (P:157-243 [Triangle counting], P:283-288 [k-Truss]): support(u,v) =
+// |N(u) ∩ N(v)|; the triangle count is Σ support / 3.  Here every triangle
+// is found exactly once in the rank-oriented DAG (Alg. 3's L·U masked by A,
+// P:230-243, after relabelling by (degree, id)): for ranks u < v < w the
+// triangle is found at its middle vertex v, by its lowest vertex u:
+//
+//   for each v with d+(v) > 0:  H = hash of N+(v) in shared memory
+//     for each in-edge u -> v:  for each w in N+(u) after v (the suffix):
+//        w ∈ H  <=>  triangle {u, v, w}
+//
+// Only the suffix of N+(u) past v can meet N+(v) (its entries all rank
+// above v), so the streamed volume is Σ_x C(d+(x), 2) wedges instead of the
+// full Σ d-·d+ (DESIGN.md "Kernels").  Per-edge support credits the three
+// edges of each triangle found:  (u,v) via a per-in-edge shared counter,
+// (v,w) via a per-hash-slot shared counter, (u,w) via one global atomic.
+//
+// Task classes by d+(v): 0 warp task, 64-slot table; 1 warp task,
+// 512-slot table; 2 block task, 8192-slot table; 3 warp task, binary search
+// of N+(v) in global memory (d+(v) > 4096, rare).  Tasks are (v, in-edge
+// range) cut by an exclusive scan of a per-in-edge cost so every task holds
+// about task_chunk wedges; the same cut points give the multi-GPU 1D
+// partition.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+
+#include "gc_internal.cuh"
+
+namespace gcx {
+
+namespace {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr int kOvh = 2;                     // per in-edge overhead in the cost model
+constexpr int kD0 = 32, kD1 = 256, kD2 = 4096;
+constexpr int kTS0 = 64, kTS1 = 512, kTS2 = 8192;
+constexpr int kWarps = 8;                   // 256 threads per block
+
+__device__ __forceinline__ int task_class(int64_t d, int force) {
+    int c = d <= kD0 ? 0 : d <= kD1 ? 1 : d <= kD2 ? 2 : 3;
+    return c > force ? c : force;
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t w, int lg) { return (w * 0x9E3779B1u) >> (32 - lg); }
+
+__device__ __forceinline__ int table_lg(int d, int max_lg) {
+    int lg = 5;                                 // >= 32 slots, load factor <= 1/2
+    while ((1 << lg) < 2 * d && lg < max_lg) ++lg;
+    return lg;
+}
+
+// ------------------------------------------------------------ task build --
+__global__ void k_in_cost(const int32_t* __restrict__ in_pos, const int32_t* __restrict__ in_src,
+                          const int32_t* __restrict__ in_dst, const int64_t* __restrict__ dag_ptr, int64_t m,
+                          int64_t* __restrict__ cost) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i == m) { cost[i] = 0; continue; }
+        int v = in_dst[i];
+        int64_t dv = dag_ptr[v + 1] - dag_ptr[v];
+        int64_t len = dag_ptr[in_src[i] + 1] - (int64_t)in_pos[i] - 1;
+        cost[i] = (dv > 0 && len > 0) ? len + kOvh : 0;
+    }
+}
+
+__global__ void k_task_flags(const int64_t* __restrict__ cost, const int64_t* __restrict__ pref,
+                             const int32_t* __restrict__ in_dst, int64_t m, int64_t chunk, int64_t total, int parts,
+                             uint8_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t f = 0;
+        if (cost[i] > 0) {
+            if (i == 0 || in_dst[i - 1] != in_dst[i] || cost[i - 1] == 0) f = 1;
+            else if (pref[i] / chunk != pref[i - 1] / chunk) f = 1;
+            else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
+        }
+        flag[i] = f;
+    }
+}
+
+__global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int64_t m,
+                            const int32_t* __restrict__ in_dst, const int64_t* __restrict__ in_ptr,
+                            const int64_t* __restrict__ dag_ptr, int force, uint32_t* __restrict__ cls,
+                            uint64_t* __restrict__ packed, unsigned long long* __restrict__ hist) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ntask; j += (int64_t)gridDim.x * blockDim.x) {
+        int i0 = sel[j];
+        int v = in_dst[i0];
+        int64_t nxt = (j + 1 < ntask) ? (int64_t)sel[j + 1] : m;
+        int64_t i1 = min(nxt, in_ptr[v + 1]);
+        int k = task_class(dag_ptr[v + 1] - dag_ptr[v], force);
+        cls[j] = (uint32_t)k;
+        packed[j] = (uint64_t)(uint32_t)i0 | ((uint64_t)(uint32_t)i1 << 32);
+        atomicAdd(hist + k, 1ULL);
+    }
+}
+
+// ------------------------------------------------------- stream routine --
+// Walk the suffixes of the in-edges [i0, i1) of one task, 32 in-edges per
+// group (groups g0, g0 + gstride, ...), flattening their wedges across the
+// 32 lanes so short and long suffixes both use every lane.  probe(w) returns
+// the slot/index of w in N+(v) or -1.
+template <bool SUP, class Probe>
+__device__ __forceinline__ uint32_t stream_task(int i0, int i1, int g0, int gstride, const int32_t* __restrict__ in_pos,
+                                                const int32_t* __restrict__ in_src,
+                                                const int64_t* __restrict__ dag_ptr,
+                                                const int32_t* __restrict__ dag_col, uint32_t* __restrict__ sup,
+                                                uint32_t* seg_cnt, Probe& probe, int lane) {
+    uint32_t hits = 0;
+    for (int base = i0 + g0 * 32; base < i1; base += gstride * 32) {
+        const int i = base + lane;
+        const bool valid = i < i1;
+        int p = 0, beg = 0, len = 0;
+        if (valid) {
+            p = __ldg(in_pos + i);
+            int u = __ldg(in_src + i);
+            beg = p + 1;
+            len = (int)(__ldg(dag_ptr + u + 1) - (int64_t)beg);
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - len;
+        if (SUP) {
+            seg_cnt[lane] = 0;
+            __syncwarp();
+        }
+        for (int k = 0; k < tot; k += 32) {
+            const int t = k + lane;
+            int s = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                int e = __shfl_sync(0xffffffffu, excl, s + step);
+                if (e <= t) s += step;
+            }
+            const int es = __shfl_sync(0xffffffffu, excl, s);
+            const int bs = __shfl_sync(0xffffffffu, beg, s);
+            if (t < tot) {
+                const int q = bs + (t - es);
+                const uint32_t w = (uint32_t)__ldg(dag_col + q);
+                const int slot = probe.find(w);
+                if (slot >= 0) {
+                    ++hits;
+                    if (SUP) {
+                        atomicAdd(seg_cnt + s, 1u);    // role (u,v)
+                        probe.credit(slot, sup);       // role (v,w)
+                        atomicAdd(sup + q, 1u);        // role (u,w)
+                    }
+                }
+            }
+        }
+        if (SUP) {
+            __syncwarp();
+            if (valid && seg_cnt[lane]) atomicAdd(sup + p, seg_cnt[lane]);
+            __syncwarp();
+        }
+    }
+    return hits;
+}
+
+// Shared-memory open-addressing table of N+(v): keys = rank ids, vals =
+// index j within N+(v), cnt = (v,w)-role credits.
+template <bool SUP>
+struct SmemHash {
+    uint32_t* keys;
+    int32_t* vals;
+    uint32_t* cnt;
+    int lg;
+    uint32_t mask;
+    __device__ __forceinline__ int find(uint32_t w) const {
+        uint32_t h = hash_slot(w, lg);
+        while (true) {
+            uint32_t k = keys[h];
+            if (k == w) return (int)h;
+            if (k == kEmpty) return -1;
+            h = (h + 1) & mask;
+        }
+    }
+    __device__ __forceinline__ void credit(int slot, uint32_t*) const {
+        if (SUP) atomicAdd(cnt + slot, 1u);
+    }
+};
+
+struct KArgs {
+    const int32_t* in_pos;
+    const int32_t* in_src;
+    const int32_t* in_dst;
+    const int64_t* in_cost;
+    const int64_t* dag_ptr;
+    const int32_t* dag_col;
+    const uint64_t* tasks;      // packed (i0, i1), this class's slice
+    int64_t ntask;
+    int64_t total_cost;
+    int parts, owner;           // skip tasks not owned by `owner` of `parts`
+    uint32_t* sup;
+    unsigned long long* count;
+    int* next;                  // dynamic task counter
+};
+
+__device__ __forceinline__ bool owned(const KArgs& a, int i0) {
+    if (a.parts <= 1) return true;
+    return (int)((a.in_cost[i0] * a.parts) / a.total_cost) == a.owner;
+}
+
+__device__ __forceinline__ void add_count(unsigned long long* count, uint32_t hits, int lane) {
+    unsigned long long h = hits;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0 && h) atomicAdd(count, h);
+}
+
+// ------------------------------------------------- warp-task kernel (0, 1) --
+template <int TS, bool SUP>
+__global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
+    extern __shared__ uint32_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int per_warp = SUP ? (3 * TS + 32) : TS;
+    uint32_t* keys = smem + warp * per_warp;
+    int32_t* vals = reinterpret_cast<int32_t*>(keys + TS);
+    uint32_t* cnt = keys + 2 * TS;
+    uint32_t* seg = keys + 3 * TS;
+    constexpr int max_lg = __builtin_ctz(TS);
+    uint32_t hits = 0;
+    while (true) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(a.next, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.ntask) break;
+        const uint64_t pk = a.tasks[t];
+        const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
+        if (!owned(a, i0)) continue;
+        const int v = __ldg(a.in_dst + i0);
+        const int64_t r0 = __ldg(a.dag_ptr + v);
+        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
+        const int lg = table_lg(d, max_lg);
+        const int ts = 1 << lg;
+        for (int j = lane; j < ts; j += 32) {
+            keys[j] = kEmpty;
+            if (SUP) cnt[j] = 0;
+        }
+        __syncwarp();
+        for (int j = lane; j < d; j += 32) {
+            uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
+            uint32_t h = hash_slot(w, lg);
+            while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
+            if (SUP) vals[h] = j;
+        }
+        __syncwarp();
+        SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
+        hits += stream_task<SUP>(i0, i1, 0, 1, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, seg, H, lane);
+        if (SUP) {
+            __syncwarp();
+            for (int j = lane; j < ts; j += 32)
+                if (cnt[j]) atomicAdd(a.sup + r0 + vals[j], cnt[j]);
+        }
+        __syncwarp();
+    }
+    add_count(a.count, hits, lane);
+}
+
+// ------------------------------------------------- block-task kernel (2) --
+template <bool SUP>
+__global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
+    extern __shared__ uint32_t smem[];
+    __shared__ int s_task;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* keys = smem;
+    int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
+    uint32_t* cnt = smem + 2 * kTS2;
+    uint32_t* seg = smem + (SUP ? 3 * kTS2 : kTS2) + warp * 32;
+    constexpr int max_lg = __builtin_ctz(kTS2);
+    uint32_t hits = 0;
+    while (true) {
+        if (threadIdx.x == 0) s_task = atomicAdd(a.next, 1);
+        __syncthreads();
+        const int t = s_task;
+        __syncthreads();
+        if (t >= a.ntask) break;
+        const uint64_t pk = a.tasks[t];
+        const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
+        if (!owned(a, i0)) continue;
+        const int v = __ldg(a.in_dst + i0);
+        const int64_t r0 = __ldg(a.dag_ptr + v);
+        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
+        const int lg = table_lg(d, max_lg);
+        const int ts = 1 << lg;
+        for (int j = threadIdx.x; j < ts; j += blockDim.x) {
+            keys[j] = kEmpty;
+            if (SUP) cnt[j] = 0;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < d; j += blockDim.x) {
+            uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
+            uint32_t h = hash_slot(w, lg);
+            while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
+            if (SUP) vals[h] = j;
+        }
+        __syncthreads();
+        SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
+        hits += stream_task<SUP>(i0, i1, warp, kWarps, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, seg, H, lane);
+        __syncthreads();
+        if (SUP) {
+            for (int j = threadIdx.x; j < ts; j += blockDim.x)
+                if (cnt[j]) atomicAdd(a.sup + r0 + vals[j], cnt[j]);
+            __syncthreads();
+        }
+    }
+    add_count(a.count, hits, lane);
+}
+
+// ------------------------------------------ binary-search kernel (3) --
+struct GlobalProbe {
+    const int32_t* row;
+    int d;
+    int64_t r0;
+    __device__ __forceinline__ int find(uint32_t w) const {
+        int lo = 0, hi = d;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if ((uint32_t)__ldg(row + mid) < w) lo = mid + 1; else hi = mid;
+        }
+        return (lo < d && (uint32_t)__ldg(row + lo) == w) ? lo : -1;
+    }
+    __device__ __forceinline__ void credit(int j, uint32_t* sup) const { atomicAdd(sup + r0 + j, 1u); }
+};
+
+template <bool SUP>
+__global__ void __launch_bounds__(256) k_tc_search(KArgs a) {
+    __shared__ uint32_t segs[kWarps * 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t hits = 0;
+    while (true) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(a.next, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.ntask) break;
+        const uint64_t pk = a.tasks[t];
+        const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
+        if (!owned(a, i0)) continue;
+        const int v = __ldg(a.in_dst + i0);
+        const int64_t r0 = __ldg(a.dag_ptr + v);
+        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
+        GlobalProbe G{a.dag_col + r0, d, r0};
+        hits += stream_task<SUP>(i0, i1, 0, 1, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, segs + warp * 32, G,
+                                 lane);
+    }
+    add_count(a.count, hits, lane);
+}
+
+__global__ void k_scatter_u32(const uint32_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
+                              uint32_t* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
+        out[eid[p]] = vals[p];
+}
+
+template <class K>
+int occupancy_grid(K kernel, size_t smem) {
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, 256, smem) != cudaSuccess || blocks < 1) {
+        cudaGetLastError();
+        blocks = 1;
+    }
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return blocks * sms;
+}
+
+}  // namespace
+
+int prepare_tasks(gc_ctx* c) {
+    const int64_t m = c->m;
+    c->tasks_ready = false;
+    for (int k = 0; k < 4; ++k) c->ntask[k] = 0;
+    for (int k = 0; k < 5; ++k) c->task_off[k] = 0;
+    c->total_cost = 0;
+    c->task_parts = c->loop_parts > 0 ? c->loop_parts : c->nranks;
+    if (m == 0) {
+        c->tasks_ready = true;
+        return GC_OK;
+    }
+    GC_TRY(ensure(c, c->in_cost, (size_t)(m + 1) * 8));
+    GC_TRY(ensure(c, c->tmp_a, (size_t)(m + 1) * 8));      // cost, then packed tasks (sorted)
+    GC_TRY(ensure(c, c->tmp_b, (size_t)(m + 1) * 8));      // packed tasks (unsorted)
+    GC_TRY(ensure(c, c->task_i0, (size_t)(m + 1) * 8));    // final packed tasks
+    GC_TRY(ensure(c, c->vals_a, (size_t)(m + 1) * 4));     // flags (uint8) / selected indices
+    GC_TRY(ensure(c, c->vals_b, (size_t)(m + 1) * 4));
+    GC_TRY(ensure(c, c->keys_a, (size_t)(m + 1) * 8));
+    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(host_scratch(c, 4096));
+    int64_t* h = static_cast<int64_t*>(c->hpin);
+    int64_t* cost = c->tmp_a.as<int64_t>();
+    GC_LAUNCH(c, k_in_cost, grid_for(m + 1), kThreads, 0, c->in_pos.as<int32_t>(), c->in_src.as<int32_t>(),
+              c->in_dst.as<int32_t>(), c->dag_ptr.as<int64_t>(), m, cost);
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cost, c->in_cost.as<int64_t>(), m + 1, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cost, c->in_cost.as<int64_t>(), m + 1, c->stream));
+    c->stats.lib_launches += 2;
+    GC_CUDA(c, cudaMemcpyAsync(h, c->in_cost.as<int64_t>() + m, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    c->total_cost = h[0];
+    if (c->total_cost == 0) {
+        c->tasks_ready = true;
+        return GC_OK;
+    }
+    uint8_t* flags = reinterpret_cast<uint8_t*>(c->vals_b.p);
+    GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, cost, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(), m,
+              c->task_chunk, c->total_cost, c->task_parts, flags);
+    int32_t* sel = c->vals_a.as<int32_t>();
+    int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 128);
+    thrust::counting_iterator<int32_t> iota(0);
+    tmp = 0;
+    GC_CUDA(c, cub::DeviceSelect::Flagged(nullptr, tmp, iota, flags, sel, d_nsel, m, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, flags, sel, d_nsel, m, c->stream));
+    c->stats.lib_launches += 2;
+    GC_CUDA(c, cudaMemcpyAsync(h, d_nsel, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    const int64_t nt = h[0];
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 160);
+    GC_CUDA(c, cudaMemsetAsync(hist, 0, 4 * 8, c->stream));
+    uint32_t* cls = reinterpret_cast<uint32_t*>(c->keys_a.p);
+    uint32_t* cls_sorted = cls + (m + 1);
+    GC_LAUNCH(c, k_task_fill, grid_for(nt), kThreads, 0, sel, nt, m, c->in_dst.as<int32_t>(), c->in_ptr.as<int64_t>(),
+              c->dag_ptr.as<int64_t>(), c->force_class, cls, c->tmp_b.as<uint64_t>(), hist);
+    tmp = 0;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
+                                               c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
+                                               c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
+    c->stats.lib_launches += 3;
+    GC_CUDA(c, cudaMemcpyAsync(h, hist, 4 * 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    int64_t off = 0;
+    for (int k = 0; k < 4; ++k) {
+        c->ntask[k] = h[k];
+        c->task_off[k] = off;
+        off += h[k];
+    }
+    c->task_off[4] = off;
+    c->tasks_ready = true;
+    return GC_OK;
+}
+
+// Launch every class kernel for owner `owner` of `parts`.
+template <bool SUP>
+static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* count, uint32_t* sup) {
+    int* next = reinterpret_cast<int*>(c->scal.as<char>() + 64);
+    GC_CUDA(c, cudaMemsetAsync(next, 0, 4 * sizeof(int), c->stream));
+    KArgs a{};
+    a.in_pos = c->in_pos.as<int32_t>();
+    a.in_src = c->in_src.as<int32_t>();
+    a.in_dst = c->in_dst.as<int32_t>();
+    a.in_cost = c->in_cost.as<int64_t>();
+    a.dag_ptr = c->dag_ptr.as<int64_t>();
+    a.dag_col = c->dag_col.as<int32_t>();
+    a.total_cost = c->total_cost;
+    a.parts = parts;
+    a.owner = owner;
+    a.sup = sup;
+    a.count = count;
+    const uint64_t* tasks = c->task_i0.as<uint64_t>();
+    // class 2 first (heaviest tasks), then 1, 0, 3
+    if (c->ntask[2] > 0) {
+        a.tasks = tasks + c->task_off[2];
+        a.ntask = c->ntask[2];
+        a.next = next + 2;
+        const size_t smem = (SUP ? 3 * kTS2 + kWarps * 32 : kTS2 + kWarps * 32) * sizeof(uint32_t);
+        static bool attr_set[2] = {false, false};
+        if (!attr_set[SUP]) {
+            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set[SUP] = true;
+        }
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(k_tc_block<SUP>, smem);
+        GC_LAUNCH(c, k_tc_block<SUP>, (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
+    }
+    if (c->ntask[1] > 0) {
+        a.tasks = tasks + c->task_off[1];
+        a.ntask = c->ntask[1];
+        a.next = next + 1;
+        const size_t smem = kWarps * (SUP ? 3 * kTS1 + 32 : kTS1) * sizeof(uint32_t);
+        static bool attr_set = false;
+        if (!attr_set) {
+            GC_CUDA(c, cudaFuncSetAttribute(k_tc_warp<kTS1, SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+            attr_set = true;
+        }
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(k_tc_warp<kTS1, SUP>, smem);
+        GC_LAUNCH(c, (k_tc_warp<kTS1, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
+    }
+    if (c->ntask[0] > 0) {
+        a.tasks = tasks + c->task_off[0];
+        a.ntask = c->ntask[0];
+        a.next = next + 0;
+        const size_t smem = kWarps * (SUP ? 3 * kTS0 + 32 : kTS0) * sizeof(uint32_t);
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(k_tc_warp<kTS0, SUP>, smem);
+        GC_LAUNCH(c, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
+    }
+    if (c->ntask[3] > 0) {
+        a.tasks = tasks + c->task_off[3];
+        a.ntask = c->ntask[3];
+        a.next = next + 3;
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(k_tc_search<SUP>, 0);
+        GC_LAUNCH(c, k_tc_search<SUP>, (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, 0, a);
+    }
+    return GC_OK;
+}
+
+template <bool SUP>
+static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
+    if (!c->tasks_ready) GC_TRY(prepare_tasks(c));
+    const int parts = c->task_parts;
+    if (c->total_cost == 0) return GC_OK;
+    if (c->loop_parts > 0) {
+        for (int r = 0; r < parts; ++r) GC_TRY(launch_classes<SUP>(c, r, parts, count, sup));
+    } else {
+        GC_TRY(launch_classes<SUP>(c, c->rank, parts, count, sup));
+    }
+    return GC_OK;
+}
+
+int triangle_count(gc_ctx* c, uint64_t* out) {
+    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(host_scratch(c, 4096));
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 192);
+    GC_TRY(record(c, 2));
+    GC_CUDA(c, cudaMemsetAsync(count, 0, 8, c->stream));
+    GC_TRY(record(c, 6));
+    GC_TRY(run_all_parts<false>(c, count, nullptr));
+    GC_TRY(record(c, 7));
+    if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(count), 1));
+    GC_TRY(record(c, 3));
+    GC_CUDA(c, cudaMemcpyAsync(c->hpin, count, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    *out = *static_cast<uint64_t*>(c->hpin);
+    c->stats.tc_ms = elapsed(c, 2, 3);
+    c->stats.tc_kernel_ms = elapsed(c, 6, 7);
+    return GC_OK;
+}
+
+int support_dag(gc_ctx* c) {
+    const int64_t m = c->m;
+    GC_TRY(ensure(c, c->sup, (size_t)m * 4));
+    GC_TRY(ensure(c, c->scal, 256));
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 200);
+    GC_CUDA(c, cudaMemsetAsync(c->sup.p, 0, (size_t)m * 4, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(count, 0, 8, c->stream));
+    GC_TRY(record(c, 6));
+    GC_TRY(run_all_parts<true>(c, count, c->sup.as<uint32_t>()));
+    GC_TRY(record(c, 7));
+    if (c->nccl) GC_TRY(allreduce_u32(c, c->sup.as<uint32_t>(), (size_t)m));
+    return GC_OK;
+}
+
+int scatter_canonical_u32(gc_ctx* c, const uint32_t* dag_vals, uint32_t* out) {
+    const int64_t m = c->m;
+    if (m == 0) return GC_OK;
+    GC_LAUNCH(c, k_scatter_u32, grid_for(m), kThreads, 0, dag_vals, c->dag_eid.as<int32_t>(), m, out);
+    return GC_OK;
+}
+
+}  // namespace gcx

@@ -1,0 +1,297 @@
+"""GPU parity: libgc (through its C ABI) vs the CPU oracle, element by element.
+
+Integer work, so the bar is bit-exact: triangle counts, per-edge supports,
+k-truss masks and trussness must equal the oracle's on the same seeded
+inputs.  Sizes span several task tiles and ragged tails; every kernel class
+is forced over whole graphs; loopback partitions check the multi-GPU split.
+"""
+from __future__ import annotations
+
+import hashlib
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def gcmod(gc_lib_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("-m gpu tests need a CUDA device")
+    from paper_1708_06866_b200 import gc
+    return gc
+
+
+@pytest.fixture(scope="module")
+def ctx(gcmod):
+    c = gcmod.Context(0)
+    yield c
+    c.close()
+
+
+def run_gpu(ctx, u, v):
+    ctx.load_edges(u, v)
+    ctx.build_csr()
+    return ctx
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def random_graph(n, p, rng):
+    iu, ju = np.triu_indices(n, 1)
+    keep = rng.random(iu.size) < p
+    u, v = iu[keep].astype(np.int32), ju[keep].astype(np.int32)
+    flip = rng.random(u.size) < 0.5
+    return np.where(flip, v, u), np.where(flip, u, v)
+
+
+def check_all(ctx, u, v, ks=(3, 4, 5), decomposition=True):
+    g = oracle.OracleGraph(u, v)
+    run_gpu(ctx, u, v)
+    assert ctx.num_vertices() == g.n
+    assert ctx.num_edges() == g.m
+    cu, cv = ctx.get_edges()
+    assert np.array_equal(cu, g.cu) and np.array_equal(cv, g.cv)
+    T = g.triangle_count()
+    assert ctx.triangle_count() == T
+    sup = ctx.edge_support()
+    assert np.array_equal(sup, g.support())
+    for k in ks:
+        mask, m_alive = ctx.ktruss(k)
+        want, _ = g.ktruss(k)
+        assert np.array_equal(mask, want), k
+        assert m_alive == int(want.sum())
+    if decomposition:
+        tau, kmax = ctx.truss_decomposition()
+        want_tau, want_kmax = g.truss_decomposition()
+        assert np.array_equal(tau, want_tau)
+        assert kmax == want_kmax
+    return g
+
+
+# ------------------------------------------------------------ paper examples --
+@pytest.mark.parametrize("fixture", ["fig1_diamond.json", "k4_ear.json", "pendant_triangle.json"])
+def test_golden_examples(ctx, fixture):
+    d = json.load(open(os.path.join(GOLDEN, fixture)))
+    run_gpu(ctx, np.array(d["raw_u"], np.int32), np.array(d["raw_v"], np.int32))
+    cu, cv = ctx.get_edges()
+    assert cu.tolist() == d["canonical_u"] and cv.tolist() == d["canonical_v"]
+    assert ctx.triangle_count() == d["triangles"]
+    assert ctx.edge_support().tolist() == d["support"]
+    for k, mask in d["ktruss"].items():
+        assert ctx.ktruss(int(k))[0].tolist() == mask
+    tau, kmax = ctx.truss_decomposition()
+    assert tau.tolist() == d["trussness"] and kmax == d["kmax"]
+
+
+# ---------------------------------------------------------- degenerate cases --
+def test_empty_input(ctx):
+    run_gpu(ctx, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    assert ctx.num_vertices() == 0 and ctx.num_edges() == 0
+    assert ctx.triangle_count() == 0
+    assert ctx.edge_support().size == 0
+    mask, ma = ctx.ktruss(3)
+    assert mask.size == 0 and ma == 0
+    tau, kmax = ctx.truss_decomposition()
+    assert tau.size == 0 and kmax == 0
+
+
+def test_only_self_loops(ctx):
+    run_gpu(ctx, np.array([4, 4, 1], np.int32), np.array([4, 4, 1], np.int32))
+    assert ctx.num_vertices() == 5 and ctx.num_edges() == 0
+    assert ctx.triangle_count() == 0
+    assert ctx.truss_decomposition()[1] == 0
+
+
+def test_single_edge_and_duplicates(ctx):
+    run_gpu(ctx, np.array([7, 3, 7, 3], np.int32), np.array([3, 7, 3, 3], np.int32))
+    assert ctx.num_edges() == 1
+    assert ctx.get_edges()[0].tolist() == [3] and ctx.get_edges()[1].tolist() == [7]
+    assert ctx.edge_support().tolist() == [0]
+    tau, kmax = ctx.truss_decomposition()
+    assert tau.tolist() == [2] and kmax == 2
+
+
+@pytest.mark.parametrize("n", [3, 4, 9, 33, 40, 257, 600])
+def test_complete_graphs(ctx, n):
+    """K_n closed form (P2): T = C(n,3), S = n-2, tau = n; n spans task classes."""
+    u, v = map(np.array, zip(*itertools.combinations(range(n), 2)))
+    run_gpu(ctx, u.astype(np.int32), v.astype(np.int32))
+    assert ctx.triangle_count() == math.comb(n, 3)
+    assert np.all(ctx.edge_support() == n - 2)
+    assert ctx.ktruss(n)[1] == n * (n - 1) // 2
+    assert ctx.ktruss(n + 1)[1] == 0
+    if n <= 257:
+        tau, kmax = ctx.truss_decomposition()
+        assert np.all(tau == n) and kmax == n
+
+
+def test_star_cycle_tree(ctx):
+    rng = np.random.default_rng(3)
+    cases = [([0] * 5000, list(range(1, 5001))),
+             (list(range(1000)), [(i + 1) % 1000 for i in range(1000)]),
+             ([int(rng.integers(0, i)) for i in range(1, 3000)], list(range(1, 3000)))]
+    for u, v in cases:
+        run_gpu(ctx, np.array(u, np.int32), np.array(v, np.int32))
+        assert ctx.triangle_count() == 0
+        assert not ctx.edge_support().any()
+        tau, kmax = ctx.truss_decomposition()
+        assert np.all(tau == 2) and kmax == 2
+
+
+# ----------------------------------------------------------- random graphs --
+def test_random_small_graphs(ctx):
+    rng = np.random.default_rng(11)
+    for trial in range(30):
+        n = int(rng.integers(2, 70))
+        u, v = random_graph(n, float(rng.uniform(0.05, 0.9)), rng)
+        extra = rng.integers(0, n, size=(2, 5)).astype(np.int32)   # duplicates / loops
+        u = np.concatenate([u, extra[0], extra[0]])
+        v = np.concatenate([v, extra[1], extra[0]])
+        check_all(ctx, u, v, ks=(2, 3, 4, 5, 6))
+
+
+def test_rmat_small_full(ctx):
+    for s, ef, seed in [(8, 8, 5), (11, 16, 6), (12, 4, 7)]:
+        u, v = gen.rmat(s, ef, seed=seed)
+        check_all(ctx, u, v, ks=(3, 4, 6, 9))
+
+
+def test_king_grid(ctx):
+    """Table II graphs: T = 4(M-1)^2 = Table II / 2 (reading A9)."""
+    for M in (5, 64, 256):
+        u, v = gen.king_grid(M)
+        run_gpu(ctx, u, v)
+        assert ctx.num_edges() == 2 * (M - 1) * (2 * M - 1)
+        assert ctx.triangle_count() == 4 * (M - 1) ** 2
+
+
+# ------------------------------------------------------------------ configs --
+def test_c1_full(ctx):
+    u, v = gen.CONFIGS["C1"].generate()
+    g = check_all(ctx, u, v, ks=tuple(range(2, 32)))
+    assert ctx.truss_decomposition()[1] >= 3
+
+
+def test_c2_full(ctx):
+    u, v = gen.CONFIGS["C2"].generate()
+    check_all(ctx, u, v, ks=(3, 4), decomposition=True)
+
+
+def test_c3_tc_support_and_ktruss(ctx):
+    golden = os.path.join(GOLDEN, "c3_expected.json")
+    u, v = gen.CONFIGS["C3"].generate()
+    run_gpu(ctx, u, v)
+    if os.path.exists(golden):
+        d = json.load(open(golden))
+        assert ctx.num_edges() == d["m"]
+        assert ctx.triangle_count() == d["triangles"]
+        assert sha(ctx.edge_support()) == d["support_sha256"]
+        for k in (3, 4, 5, 6):
+            mask, ma = ctx.ktruss(k)
+            assert ma == d["ktruss_size"][str(k)]
+            assert sha(mask) == d["ktruss_sha256"][str(k)]
+    else:
+        g = oracle.OracleGraph(u, v)
+        assert ctx.triangle_count() == g.triangle_count()
+        assert np.array_equal(ctx.edge_support(), g.support())
+
+
+# ------------------------------------------------------- kernel class forcing --
+@pytest.mark.parametrize("force", [0, 1, 2, 3])
+def test_forced_classes(ctx, gcmod, force):
+    """Every intersection variant, forced over whole graphs."""
+    u1, v1 = gen.CONFIGS["C1"].generate()
+    u2, v2 = gen.rmat(13, 16, seed=9)
+    try:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, force)
+        for u, v in [(u1, v1), (u2, v2)]:
+            g = oracle.OracleGraph(u, v)
+            run_gpu(ctx, u, v)
+            assert ctx.triangle_count() == g.triangle_count()
+            assert np.array_equal(ctx.edge_support(), g.support())
+    finally:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
+
+
+def test_task_chunk_sizes(ctx, gcmod):
+    u, v = gen.rmat(12, 16, seed=13)
+    g = oracle.OracleGraph(u, v)
+    want = g.support()
+    try:
+        for chunk in (32, 100, 1000, 1 << 20):
+            ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, chunk)
+            run_gpu(ctx, u, v)
+            assert np.array_equal(ctx.edge_support(), want)
+    finally:
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+
+
+def test_large_clique_all_classes(ctx):
+    """K_4200: out-degrees span every class including the >4096 binary-search one."""
+    n = 4200
+    iu, ju = np.triu_indices(n, 1)
+    run_gpu(ctx, iu.astype(np.int32), ju.astype(np.int32))
+    assert ctx.triangle_count() == math.comb(n, 3)
+    assert np.all(ctx.edge_support() == n - 2)
+
+
+# -------------------------------------------------- loopback partitions (T3) --
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_loopback_partitions(gcmod, parts):
+    u, v = gen.rmat(13, 16, seed=17)
+    g = oracle.OracleGraph(u, v)
+    with gcmod.Context(0) as c:
+        c.comm_init_loopback(parts)
+        c.load_edges(u, v)
+        c.build_csr()
+        assert c.triangle_count() == g.triangle_count()
+        assert np.array_equal(c.edge_support(), g.support())
+        want, _ = g.ktruss(5)
+        assert np.array_equal(c.ktruss(5)[0], want)
+
+
+# --------------------------------------------------- API / pointer kinds ----
+def test_device_pointers_and_determinism(ctx):
+    import torch
+    u, v = gen.rmat(12, 16, seed=21)
+    g = oracle.OracleGraph(u, v)
+    du = torch.from_numpy(u).cuda()
+    dv = torch.from_numpy(v).cuda()
+    ctx.load_edges(du, dv)
+    ctx.build_csr()
+    m = ctx.num_edges()
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    ctx.edge_support(out.view(torch.int32))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), g.support())
+    first = ctx.edge_support()
+    for _ in range(3):
+        assert np.array_equal(ctx.edge_support(), first)
+        assert ctx.triangle_count() == g.triangle_count()
+
+
+def test_errors(ctx, gcmod):
+    with pytest.raises(gcmod.GcError) as e:
+        run_gpu(ctx, np.array([0, -1], np.int32), np.array([1, 2], np.int32))
+    assert e.value.code == gcmod.GC_ERR_INVALID
+    run_gpu(ctx, np.array([0, 1], np.int32), np.array([1, 2], np.int32))
+    with pytest.raises(gcmod.GcError) as e:
+        ctx.ktruss(1)
+    assert e.value.code == gcmod.GC_ERR_INVALID
+    with gcmod.Context(0) as c2:
+        with pytest.raises(gcmod.GcError) as e:
+            c2.triangle_count()
+        assert e.value.code == gcmod.GC_ERR_STATE
