@@ -151,7 +151,11 @@ typedef enum gc_option {
     GC_OPT_FORCE_CLASS = 1,   /* -1 auto; 0..3 force every oriented edge through one
                                  intersection kernel class */
     GC_OPT_TASK_CHUNK = 2,    /* wedge budget per intersection task (default 4096) */
-    GC_OPT_TIMING = 3         /* 1: record CUDA events per phase (default 1) */
+    GC_OPT_TIMING = 3,        /* 1: record CUDA events per phase (default 1) */
+    GC_OPT_LONG_SEG = 5,      /* suffixes at least this long take the warp-vector path
+                                 (default 48; 2^30 disables it; testing) */
+    GC_OPT_BLOCK_BITMAP = 4,  /* 1: heavy-head kernel may use the rank-window bitmap
+                                 (default); 0: always its hash table (testing) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 
@@ -175,6 +179,7 @@ typedef struct gc_stats {
     int64_t q_in;             /* sum d-(x) d+(x) */
     int64_t max_out_degree;   /* max d+ */
     int64_t max_degree;       /* max d */
+    int64_t tasks[4];         /* intersection tasks per kernel class (last build) */
 } gc_stats;
 int gc_get_stats(const gc_ctx* ctx, gc_stats* out);
 int gc_reset_stats(gc_ctx* ctx);

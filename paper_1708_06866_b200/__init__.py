@@ -9,6 +9,7 @@ from .gc import (  # noqa: F401
     GC_OPT_FORCE_CLASS,
     GC_OPT_TASK_CHUNK,
     GC_OPT_TIMING,
+    GC_OPT_BLOCK_BITMAP,
     Context,
     GcError,
     init_distributed,

@@ -238,7 +238,7 @@ int build_csr(gc_ctx* c) {
     GC_TRY(ensure(c, c->rank_of, (size_t)n * 4));
     GC_TRY(ensure(c, c->dag_ptr, (size_t)(n + 1) * 8));
     GC_TRY(ensure(c, c->in_ptr, (size_t)(n + 1) * 8));
-    GC_TRY(ensure(c, c->dag_col, (size_t)m * 4));
+    GC_TRY(ensure(c, c->dag_col, (size_t)m * 4 + 64));   // +64: 16-byte vector loads may read past a row end
     GC_TRY(ensure(c, c->dag_src, (size_t)m * 4));
     GC_TRY(ensure(c, c->dag_eid, (size_t)m * 4));
     GC_TRY(ensure(c, c->in_pos, (size_t)m * 4));

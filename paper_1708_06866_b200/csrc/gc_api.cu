@@ -339,6 +339,13 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
                 GC_TRY(sync(c));
             }
             return GC_OK;
+        case GC_OPT_LONG_SEG:
+            if (value < 1) return fail(c, GC_ERR_INVALID, "long segment threshold must be >= 1");
+            c->long_seg = value > (1 << 30) ? (1 << 30) : (int)value;
+            return GC_OK;
+        case GC_OPT_BLOCK_BITMAP:
+            c->block_bitmap = value ? 1 : 0;
+            return GC_OK;
         case GC_OPT_TIMING:
             c->timing = value ? 1 : 0;
             return GC_OK;

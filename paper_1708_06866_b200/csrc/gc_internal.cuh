@@ -57,6 +57,8 @@ struct gc_ctx {
     int force_class = -1;
     int64_t task_chunk = 4096;
     int timing = 1;
+    int block_bitmap = 1;
+    int long_seg = 48;
 
     // raw input (a1)
     gcx::Buf raw_u, raw_v;

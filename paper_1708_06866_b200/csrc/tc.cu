@@ -68,14 +68,23 @@ __global__ void k_in_cost(const int32_t* __restrict__ in_pos, const int32_t* __r
     }
 }
 
-__global__ void k_task_flags(const int64_t* __restrict__ cost, const int64_t* __restrict__ pref,
-                             const int32_t* __restrict__ in_dst, int64_t m, int64_t chunk, int64_t total, int parts,
-                             uint8_t* __restrict__ flag) {
+// A task starts at the first in-edge of every head v that has work, and
+// wherever the running cost crosses a multiple of the class's chunk or an
+// owner boundary (multi-GPU cut).  Zero-cost in-edges (empty suffix) stay
+// inside the surrounding task.
+__global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __restrict__ in_dst,
+                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ dag_ptr, int64_t m,
+                             int64_t chunk, int64_t total, int parts, int force, uint8_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = in_dst[i];
+        const int64_t s = in_ptr[v], e = in_ptr[v + 1];
+        const int64_t dv = dag_ptr[v + 1] - dag_ptr[v];
         uint8_t f = 0;
-        if (cost[i] > 0) {
-            if (i == 0 || in_dst[i - 1] != in_dst[i] || cost[i - 1] == 0) f = 1;
-            else if (pref[i] / chunk != pref[i - 1] / chunk) f = 1;
+        if (dv > 0 && pref[e] > pref[s]) {
+            // block-class tasks get 8x the budget (8 warps share one table)
+            const int64_t ch = task_class(dv, force) == 2 ? chunk * kWarps : chunk;
+            if (i == s) f = 1;
+            else if (pref[i] / ch != pref[i - 1] / ch) f = 1;
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
         }
         flag[i] = f;
@@ -99,18 +108,23 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
 }
 
 // ------------------------------------------------------- stream routine --
-// Walk the suffixes of the in-edges [i0, i1) of one task, 32 in-edges per
-// group (groups g0, g0 + gstride, ...), flattening their wedges across the
-// 32 lanes so short and long suffixes both use every lane.  probe(w) returns
-// the slot/index of w in N+(v) or -1.
-template <bool SUP, class Probe>
-__device__ __forceinline__ uint32_t stream_task(int i0, int i1, int g0, int gstride, const int32_t* __restrict__ in_pos,
+// Walk the suffixes of the in-edges [i0, i1), 32 in-edges per group,
+// flattening their wedges across the 32 lanes so short and long suffixes
+// both use every lane.  With CLIP, only the wedges whose cost units fall in
+// [ca, cb) are visited: in-edge i owns cost units [in_cost[i], in_cost[i] +
+// kOvh + len) and its wedge j sits at unit in_cost[i] + kOvh + j, so disjoint
+// unit ranges split a task's wedges exactly (the block kernel gives each
+// warp one eighth).  probe.find(w) returns the slot/index of w in N+(v) or -1.
+template <bool SUP, bool CLIP, class Probe>
+__device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int64_t cb,
+                                                const int32_t* __restrict__ in_pos,
                                                 const int32_t* __restrict__ in_src,
+                                                const int64_t* __restrict__ in_cost,
                                                 const int64_t* __restrict__ dag_ptr,
                                                 const int32_t* __restrict__ dag_col, uint32_t* __restrict__ sup,
-                                                uint32_t* seg_cnt, Probe& probe, int lane) {
+                                                uint32_t* seg_cnt, Probe& probe, int lane, int long_seg) {
     uint32_t hits = 0;
-    for (int base = i0 + g0 * 32; base < i1; base += gstride * 32) {
+    for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
         const bool valid = i < i1;
         int p = 0, beg = 0, len = 0;
@@ -119,7 +133,50 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int g0, int gstr
             int u = __ldg(in_src + i);
             beg = p + 1;
             len = (int)(__ldg(dag_ptr + u + 1) - (int64_t)beg);
+            if (CLIP) {
+                const int64_t w0 = __ldg(in_cost + i) + kOvh;
+                int64_t lo = ca - w0, hi = cb - w0;
+                lo = lo < 0 ? 0 : (lo > len ? len : lo);
+                hi = hi < 0 ? 0 : (hi > len ? len : hi);
+                beg += (int)lo;
+                len = (int)(hi - lo);
+            }
         }
+        // Long suffixes (the bulk of the wedges): one at a time with the whole
+        // warp, 16-byte vector loads, no segment search.
+        unsigned longs = __ballot_sync(0xffffffffu, len >= long_seg);
+        while (longs) {
+            const int s = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const int b = __shfl_sync(0xffffffffu, beg, s);
+            const int e = b + __shfl_sync(0xffffffffu, len, s);
+            uint32_t seg_hits = 0;
+            for (int q0 = (b & ~3) + lane * 4; q0 < e; q0 += 128) {
+                const int4 w4 = __ldg(reinterpret_cast<const int4*>(dag_col + q0));
+                const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int q = q0 + k;
+                    if (q >= b && q < e) {
+                        const int slot = probe.find((uint32_t)wv[k]);
+                        if (slot >= 0) {
+                            ++seg_hits;
+                            if (SUP) {
+                                probe.credit(slot, sup);       // role (v,w)
+                                atomicAdd(sup + q, 1u);        // role (u,w)
+                            }
+                        }
+                    }
+                }
+            }
+            hits += seg_hits;
+            if (SUP) {
+                const uint32_t tot_hits = __reduce_add_sync(0xffffffffu, seg_hits);
+                const int ps = __shfl_sync(0xffffffffu, p, s);
+                if (lane == 0 && tot_hits) atomicAdd(sup + ps, tot_hits);   // role (u,v)
+            }
+        }
+        if (len >= long_seg) len = 0;
         int incl = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -128,10 +185,6 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int g0, int gstr
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         const int excl = incl - len;
-        if (SUP) {
-            seg_cnt[lane] = 0;
-            __syncwarp();
-        }
         for (int k = 0; k < tot; k += 32) {
             const int t = k + lane;
             int s = 0;
@@ -142,26 +195,32 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int g0, int gstr
             }
             const int es = __shfl_sync(0xffffffffu, excl, s);
             const int bs = __shfl_sync(0xffffffffu, beg, s);
+            const int ps = SUP ? __shfl_sync(0xffffffffu, p, s) : 0;
+            bool hit = false;
             if (t < tot) {
                 const int q = bs + (t - es);
                 const uint32_t w = (uint32_t)__ldg(dag_col + q);
                 const int slot = probe.find(w);
                 if (slot >= 0) {
+                    hit = true;
                     ++hits;
                     if (SUP) {
-                        atomicAdd(seg_cnt + s, 1u);    // role (u,v)
                         probe.credit(slot, sup);       // role (v,w)
                         atomicAdd(sup + q, 1u);        // role (u,w)
                     }
                 }
             }
-        }
-        if (SUP) {
-            __syncwarp();
-            if (valid && seg_cnt[lane]) atomicAdd(sup + p, seg_cnt[lane]);
-            __syncwarp();
+            if (SUP) {
+                // role (u,v): lanes of one segment are contiguous; one atomic per segment
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const unsigned grp = __match_any_sync(hm, s);
+                    if (lane == __ffs(grp) - 1) atomicAdd(sup + ps, (uint32_t)__popc(grp));
+                }
+            }
         }
     }
+    (void)seg_cnt;
     return hits;
 }
 
@@ -202,6 +261,8 @@ struct KArgs {
     uint32_t* sup;
     unsigned long long* count;
     int* next;                  // dynamic task counter
+    uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
+    int long_seg;               // suffix length threshold of the warp-vector path
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -228,11 +289,9 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
     uint32_t* seg = keys + 3 * TS;
     constexpr int max_lg = __builtin_ctz(TS);
     uint32_t hits = 0;
-    while (true) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(a.next, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.ntask) break;
+    // static round-robin over tasks (every task's cost is bounded by the chunk)
+    const int64_t nw = (int64_t)gridDim.x * kWarps;
+    for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < a.ntask; t += nw) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
         if (!owned(a, i0)) continue;
@@ -254,7 +313,8 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
         }
         __syncwarp();
         SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
-        hits += stream_task<SUP>(i0, i1, 0, 1, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, seg, H, lane);
+        hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
+                                        seg, H, lane, a.long_seg);
         if (SUP) {
             __syncwarp();
             for (int j = lane; j < ts; j += 32)
@@ -266,49 +326,133 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
 }
 
 // ------------------------------------------------- block-task kernel (2) --
+// Heavy heads (257 <= d+(v) <= 4096).  N+(v) is held as a bitmap over the
+// rank window (v, v + 32*kBW] when its largest element fits (one LDS per
+// probe, no probe chains), else as the 8192-slot hash.  The task's wedges
+// are split exactly into 8 equal cost-unit slices, one per warp, so the
+// block barrier after the stream does not wait on a straggler warp.
+constexpr int kBW = 16384;   // bitmap words (64 KB): 524288 ranks
+
+template <bool SUP>
+struct SmemBitmap {
+    const uint32_t* bits;
+    const uint16_t* pre;     // SUP: index in N+(v) of the first element of each word
+    uint32_t* cnt;           // SUP: (v,w)-role credits per index j
+    uint32_t base;           // v + 1
+    uint32_t nbits;
+    __device__ __forceinline__ int find(uint32_t w) const {
+        const uint32_t x = w - base;
+        if (x >= nbits) return -1;
+        const uint32_t word = bits[x >> 5];
+        const uint32_t bit = 1u << (x & 31);
+        if (!(word & bit)) return -1;
+        if (!SUP) return 0;
+        return (int)pre[x >> 5] + __popc(word & (bit - 1));
+    }
+    __device__ __forceinline__ void credit(int j, uint32_t*) const {
+        if (SUP) atomicAdd(cnt + j, 1u);
+    }
+};
+
+// Smallest i in [lo, hi) with a[i] >= x (hi if none); one warp, 32-ary search.
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ a, int64_t lo, int64_t hi, int64_t x,
+                                                    int lane) {
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t pos = lo + lane * step;
+        const bool less = pos < hi && __ldg(a + pos) < x;
+        const int c = __popc(__ballot_sync(0xffffffffu, less));
+        const int64_t nlo = c > 0 ? lo + (int64_t)(c - 1) * step + 1 : lo;
+        const int64_t nhi = c < 32 ? min(hi, lo + (int64_t)c * step) : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    const int64_t pos = lo + lane;
+    const bool less = pos < hi && __ldg(a + pos) < x;
+    return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
 template <bool SUP>
 __global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
     extern __shared__ uint32_t smem[];
-    __shared__ int s_task;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
+    // SUP: [kBW, kBW + kBW/2) u16 prefix | hash cnt ; then kD2 bitmap-mode cnt ; then seg
+    uint32_t* bits = smem;
     uint32_t* keys = smem;
     int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
-    uint32_t* cnt = smem + 2 * kTS2;
-    uint32_t* seg = smem + (SUP ? 3 * kTS2 : kTS2) + warp * 32;
+    uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBW);
+    uint32_t* hcnt = smem + kBW;
+    uint32_t* bcnt = smem + kBW + kBW / 2;
+    uint32_t* seg = smem + (SUP ? kBW + kBW / 2 + kD2 : kBW) + warp * 32;
     constexpr int max_lg = __builtin_ctz(kTS2);
+    static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
     uint32_t hits = 0;
-    while (true) {
-        if (threadIdx.x == 0) s_task = atomicAdd(a.next, 1);
-        __syncthreads();
-        const int t = s_task;
-        __syncthreads();
-        if (t >= a.ntask) break;
+    for (int64_t t = blockIdx.x; t < a.ntask; t += gridDim.x) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
         if (!owned(a, i0)) continue;
         const int v = __ldg(a.in_dst + i0);
         const int64_t r0 = __ldg(a.dag_ptr + v);
         const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
-        const int lg = table_lg(d, max_lg);
-        const int ts = 1 << lg;
-        for (int j = threadIdx.x; j < ts; j += blockDim.x) {
-            keys[j] = kEmpty;
-            if (SUP) cnt[j] = 0;
+        const uint32_t span = (uint32_t)__ldg(a.dag_col + r0 + d - 1) - (uint32_t)v;   // max rank - v
+        const bool use_bm = span <= a.bm_bits;
+        int lg = 0, ts = 0;
+        if (use_bm) {
+            const int nwords = (int)((span + 31) >> 5);
+            for (int j = threadIdx.x; j < nwords; j += blockDim.x) bits[j] = 0u;
+            if (SUP)
+                for (int j = threadIdx.x; j < d; j += blockDim.x) bcnt[j] = 0u;
+            __syncthreads();
+            for (int j = threadIdx.x; j < d; j += blockDim.x) {
+                const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
+                atomicOr(bits + (x >> 5), 1u << (x & 31));
+                if (SUP) {
+                    const bool first = j == 0 || (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 5) != (x >> 5);
+                    if (first) pre[x >> 5] = (uint16_t)j;
+                }
+            }
+        } else {
+            lg = table_lg(d, max_lg);
+            ts = 1 << lg;
+            for (int j = threadIdx.x; j < ts; j += blockDim.x) {
+                keys[j] = kEmpty;
+                if (SUP) hcnt[j] = 0;
+            }
+            __syncthreads();
+            for (int j = threadIdx.x; j < d; j += blockDim.x) {
+                uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
+                uint32_t h = hash_slot(w, lg);
+                while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
+                if (SUP) vals[h] = j;
+            }
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < d; j += blockDim.x) {
-            uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
-            uint32_t h = hash_slot(w, lg);
-            while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
-            if (SUP) vals[h] = j;
+        // this warp's eighth of the task's cost units
+        const int64_t c0 = __ldg(a.in_cost + i0), c1 = __ldg(a.in_cost + i1);
+        const int64_t ca = c0 + (c1 - c0) * warp / kWarps, cb = c0 + (c1 - c0) * (warp + 1) / kWarps;
+        if (cb > ca) {
+            const int first = (int)warp_lower_bound(a.in_cost, i0, i1, ca + 1, lane) - 1;
+            const int end = (int)warp_lower_bound(a.in_cost, i0, i1, cb, lane);
+            if (use_bm) {
+                SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u, span};
+                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                                               a.dag_col, a.sup, seg, B, lane, a.long_seg);
+            } else {
+                SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
+                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                                               a.dag_col, a.sup, seg, H, lane, a.long_seg);
+            }
         }
-        __syncthreads();
-        SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
-        hits += stream_task<SUP>(i0, i1, warp, kWarps, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, seg, H, lane);
         __syncthreads();
         if (SUP) {
-            for (int j = threadIdx.x; j < ts; j += blockDim.x)
-                if (cnt[j]) atomicAdd(a.sup + r0 + vals[j], cnt[j]);
+            if (use_bm) {
+                for (int j = threadIdx.x; j < d; j += blockDim.x)
+                    if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
+            } else {
+                for (int j = threadIdx.x; j < ts; j += blockDim.x)
+                    if (hcnt[j]) atomicAdd(a.sup + r0 + vals[j], hcnt[j]);
+            }
             __syncthreads();
         }
     }
@@ -336,11 +480,8 @@ __global__ void __launch_bounds__(256) k_tc_search(KArgs a) {
     __shared__ uint32_t segs[kWarps * 32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t hits = 0;
-    while (true) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(a.next, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.ntask) break;
+    const int64_t nw = (int64_t)gridDim.x * kWarps;
+    for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < a.ntask; t += nw) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
         if (!owned(a, i0)) continue;
@@ -348,8 +489,8 @@ __global__ void __launch_bounds__(256) k_tc_search(KArgs a) {
         const int64_t r0 = __ldg(a.dag_ptr + v);
         const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
         GlobalProbe G{a.dag_col + r0, d, r0};
-        hits += stream_task<SUP>(i0, i1, 0, 1, a.in_pos, a.in_src, a.dag_ptr, a.dag_col, a.sup, segs + warp * 32, G,
-                                 lane);
+        hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
+                                        segs + warp * 32, G, lane, a.long_seg);
     }
     add_count(a.count, hits, lane);
 }
@@ -413,8 +554,9 @@ int prepare_tasks(gc_ctx* c) {
         return GC_OK;
     }
     uint8_t* flags = reinterpret_cast<uint8_t*>(c->vals_b.p);
-    GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, cost, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(), m,
-              c->task_chunk, c->total_cost, c->task_parts, flags);
+    GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(),
+              c->in_ptr.as<int64_t>(), c->dag_ptr.as<int64_t>(), m, c->task_chunk, c->total_cost, c->task_parts,
+              c->force_class, flags);
     int32_t* sel = c->vals_a.as<int32_t>();
     int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 128);
     thrust::counting_iterator<int32_t> iota(0);
@@ -446,6 +588,7 @@ int prepare_tasks(gc_ctx* c) {
     int64_t off = 0;
     for (int k = 0; k < 4; ++k) {
         c->ntask[k] = h[k];
+        c->stats.tasks[k] = h[k];
         c->task_off[k] = off;
         off += h[k];
     }
@@ -471,13 +614,15 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.owner = owner;
     a.sup = sup;
     a.count = count;
+    a.bm_bits = c->block_bitmap ? (uint32_t)kBW * 32u : 0u;
+    a.long_seg = c->long_seg;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
     // class 2 first (heaviest tasks), then 1, 0, 3
     if (c->ntask[2] > 0) {
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         a.next = next + 2;
-        const size_t smem = (SUP ? 3 * kTS2 + kWarps * 32 : kTS2 + kWarps * 32) * sizeof(uint32_t);
+        const size_t smem = (SUP ? kBW + kBW / 2 + kD2 + kWarps * 32 : kBW + kWarps * 32) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
             GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -33,6 +33,8 @@ _NAMES = {0: "GC_OK", 1: "GC_ERR_INVALID", 2: "GC_ERR_STATE", 3: "GC_ERR_RANGE",
 GC_OPT_FORCE_CLASS = 1
 GC_OPT_TASK_CHUNK = 2
 GC_OPT_TIMING = 3
+GC_OPT_BLOCK_BITMAP = 4
+GC_OPT_LONG_SEG = 5
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -51,7 +53,7 @@ class gc_stats(ctypes.Structure):
         ("launches", ctypes.c_int64), ("lib_launches", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("wedges", ctypes.c_int64),
         ("q_out", ctypes.c_int64), ("q_in", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
-        ("max_degree", ctypes.c_int64),
+        ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),
     ]
 
 
@@ -248,7 +250,9 @@ class Context:
     def stats(self) -> dict:
         s = gc_stats()
         self._check(self._L.gc_get_stats(self._h, ctypes.byref(s)))
-        return {name: getattr(s, name) for name, _ in gc_stats._fields_}
+        out = {name: getattr(s, name) for name, _ in gc_stats._fields_}
+        out["tasks"] = list(out["tasks"])
+        return out
 
     def reset_stats(self):
         self._check(self._L.gc_reset_stats(self._h))

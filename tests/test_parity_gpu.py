@@ -227,6 +227,27 @@ def test_forced_classes(ctx, gcmod, force):
         ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
 
 
+@pytest.mark.parametrize("bitmap", [0, 1])
+def test_heavy_head_bitmap_and_hash(ctx, gcmod, bitmap):
+    """The heavy-head (class 2) kernel in both membership modes, forced on all heads."""
+    u, v = gen.rmat(13, 16, seed=19)
+    g = oracle.OracleGraph(u, v)
+    try:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, 2)
+        ctx.set_option(gcmod.GC_OPT_BLOCK_BITMAP, bitmap)
+        run_gpu(ctx, u, v)
+        assert ctx.triangle_count() == g.triangle_count()
+        assert np.array_equal(ctx.edge_support(), g.support())
+        for chunk in (32, 777):
+            ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, chunk)
+            assert ctx.triangle_count() == g.triangle_count()
+            assert np.array_equal(ctx.edge_support(), g.support())
+    finally:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
+        ctx.set_option(gcmod.GC_OPT_BLOCK_BITMAP, 1)
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+
+
 def test_task_chunk_sizes(ctx, gcmod):
     u, v = gen.rmat(12, 16, seed=13)
     g = oracle.OracleGraph(u, v)
