@@ -154,6 +154,8 @@ typedef enum gc_option {
     GC_OPT_TIMING = 3,        /* 1: record CUDA events per phase (default 1) */
     GC_OPT_LONG_SEG = 5,      /* suffixes at least this long take the warp-vector path
                                  (default 48; 2^30 disables it; testing) */
+    GC_OPT_BLOCK_BATCH = 6,   /* heavy-head kernel: consecutive tasks per block batch,
+                                 batches dealt round-robin (default 4; tuning) */
     GC_OPT_BLOCK_BITMAP = 4,  /* 1: heavy-head kernel may use the rank-window bitmap
                                  (default); 0: always its hash table (testing) */
 } gc_option;
@@ -180,6 +182,8 @@ typedef struct gc_stats {
     int64_t max_out_degree;   /* max d+ */
     int64_t max_degree;       /* max d */
     int64_t tasks[4];         /* intersection tasks per kernel class (last build) */
+    int64_t aux[8];           /* heads with d+ > 256 by rank span of N+ (<=2^17, 2^18,
+                                 2^19, more): counts [0..3], in-degree weighted [4..7] */
 } gc_stats;
 int gc_get_stats(const gc_ctx* ctx, gc_stats* out);
 int gc_reset_stats(gc_ctx* ctx);

@@ -111,8 +111,11 @@ __global__ void k_in_keys(const int32_t* __restrict__ col, const int32_t* __rest
 
 // Work-model sums over vertices: wedges = Σ C(d+,2), Q_out = Σ d+², Q_in = Σ d- d+,
 // max d+, max d.
+// Also (aux) heads with d+ > 256: rank span of N+(x) in buckets <= 2^17, 2^18,
+// 2^19, more — counts in acc[5..8], in-degree-weighted in acc[9..12].
 __global__ void k_graph_stats(const int64_t* __restrict__ dag_ptr, const int64_t* __restrict__ in_ptr,
-                              const int32_t* __restrict__ deg, int64_t n, unsigned long long* __restrict__ acc) {
+                              const int32_t* __restrict__ deg, const int32_t* __restrict__ dag_col, int64_t n,
+                              unsigned long long* __restrict__ acc) {
     unsigned long long w = 0, qo = 0, qi = 0;
     int mo = 0, md = 0;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
@@ -123,6 +126,12 @@ __global__ void k_graph_stats(const int64_t* __restrict__ dag_ptr, const int64_t
         qi += dm * dp;
         mo = max(mo, (int)dp);
         md = max(md, deg[x]);
+        if (dp > 256) {
+            const int64_t span = (int64_t)dag_col[dag_ptr[x + 1] - 1] - x;
+            const int bkt = span <= (1 << 17) ? 0 : span <= (1 << 18) ? 1 : span <= (1 << 19) ? 2 : 3;
+            atomicAdd(acc + 5 + bkt, 1ULL);
+            atomicAdd(acc + 9 + bkt, dm);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         w += __shfl_xor_sync(0xffffffffu, w, o);
@@ -179,7 +188,7 @@ int build_csr(gc_ctx* c) {
     c->n = 0;
     c->m = 0;
     c->bits = 1;
-    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(ensure(c, c->scal, 1024));
     int* d_scal = c->scal.as<int>();
     GC_TRY(host_scratch(c, 4096));
     int64_t* h = static_cast<int64_t*>(c->hpin);
@@ -282,12 +291,12 @@ int build_csr(gc_ctx* c) {
               c->in_ptr.as<int64_t>());
 
     // ---- work-model statistics (one reduction over vertices)
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(d_scal + 16);
-    GC_CUDA(c, cudaMemsetAsync(acc, 0, 5 * 8, c->stream));
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 512);
+    GC_CUDA(c, cudaMemsetAsync(acc, 0, 13 * 8, c->stream));
     if (n > 0)
         GC_LAUNCH(c, k_graph_stats, grid_for(n), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(),
-                  c->deg.as<int32_t>(), n, acc);
-    GC_CUDA(c, cudaMemcpyAsync(h, acc, 5 * 8, cudaMemcpyDeviceToHost, c->stream));
+                  c->deg.as<int32_t>(), c->dag_col.as<int32_t>(), n, acc);
+    GC_CUDA(c, cudaMemcpyAsync(h, acc, 13 * 8, cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
     c->stats.n = n;
     c->stats.m = m;
@@ -296,6 +305,7 @@ int build_csr(gc_ctx* c) {
     c->stats.q_in = h[2];
     c->stats.max_out_degree = h[3];
     c->stats.max_degree = h[4];
+    for (int k = 0; k < 8; ++k) c->stats.aux[k] = h[5 + k];
     return GC_OK;
 }
 

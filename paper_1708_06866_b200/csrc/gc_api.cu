@@ -339,12 +339,22 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
                 GC_TRY(sync(c));
             }
             return GC_OK;
+        case GC_OPT_BLOCK_BATCH:
+            if (value < 1 || value > (1 << 20)) return fail(c, GC_ERR_INVALID, "block batch must be 1..2^20");
+            c->block_batch = (int)value;
+            return GC_OK;
         case GC_OPT_LONG_SEG:
             if (value < 1) return fail(c, GC_ERR_INVALID, "long segment threshold must be >= 1");
             c->long_seg = value > (1 << 30) ? (1 << 30) : (int)value;
             return GC_OK;
         case GC_OPT_BLOCK_BITMAP:
             c->block_bitmap = value ? 1 : 0;
+            c->tasks_ready = false;   // the class of a head depends on the bitmap capacity
+            if (c->state == 2) {
+                cudaSetDevice(c->device);
+                GC_TRY(prepare_tasks(c));
+                GC_TRY(sync(c));
+            }
             return GC_OK;
         case GC_OPT_TIMING:
             c->timing = value ? 1 : 0;

@@ -59,6 +59,7 @@ struct gc_ctx {
     int timing = 1;
     int block_bitmap = 1;
     int long_seg = 48;
+    int block_batch = 32;
 
     // raw input (a1)
     gcx::Buf raw_u, raw_v;

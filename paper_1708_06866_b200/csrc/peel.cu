@@ -219,7 +219,7 @@ static int peel_setup(gc_ctx* c) {
     GC_TRY(ensure(c, c->rem, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_a, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_b, (size_t)m * 4));
-    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(ensure(c, c->scal, 1024));
     GC_TRY(host_scratch(c, 4096));
     if (m > 0) {
         GC_LAUNCH(c, k_fill_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, (uint8_t)1);

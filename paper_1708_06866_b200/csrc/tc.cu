@@ -39,12 +39,26 @@ namespace {
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kOvh = 2;                     // per in-edge overhead in the cost model
 constexpr int kD0 = 32, kD1 = 256, kD2 = 4096;
-constexpr int kTS0 = 64, kTS1 = 512, kTS2 = 8192;
+constexpr int kTS0 = 64, kTS1 = 512;
+constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB): ranks (v, v + 2^18]
+constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not fit
+constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
 
-__device__ __forceinline__ int task_class(int64_t d, int force) {
-    int c = d <= kD0 ? 0 : d <= kD1 ? 1 : d <= kD2 ? 2 : 3;
-    return c > force ? c : force;
+// Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
+// tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
+// d+ <= kD2H), 3 global binary search.  force raises the class (testing).
+__device__ __forceinline__ int head_class(const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col,
+                                          int v, int force, uint32_t bm_bits) {
+    const int64_t r0 = dag_ptr[v];
+    const int64_t d = dag_ptr[v + 1] - r0;
+    int c = d <= kD0 ? 0 : d <= kD1 ? 1 : 2;
+    if (c < force) c = force;
+    if (c == 2) {
+        const uint32_t span = d > 0 ? (uint32_t)dag_col[r0 + d - 1] - (uint32_t)v : 0u;
+        if (d > kD2 || (span > bm_bits && d > kD2H)) c = 3;
+    }
+    return c;
 }
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t w, int lg) { return (w * 0x9E3779B1u) >> (32 - lg); }
@@ -73,8 +87,9 @@ __global__ void k_in_cost(const int32_t* __restrict__ in_pos, const int32_t* __r
 // owner boundary (multi-GPU cut).  Zero-cost in-edges (empty suffix) stay
 // inside the surrounding task.
 __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __restrict__ in_dst,
-                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ dag_ptr, int64_t m,
-                             int64_t chunk, int64_t total, int parts, int force, uint8_t* __restrict__ flag) {
+                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ dag_ptr,
+                             const int32_t* __restrict__ dag_col, int64_t m, int64_t chunk, int64_t total, int parts,
+                             int force, uint32_t bm_bits, uint8_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int v = in_dst[i];
         const int64_t s = in_ptr[v], e = in_ptr[v + 1];
@@ -82,7 +97,7 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
         uint8_t f = 0;
         if (dv > 0 && pref[e] > pref[s]) {
             // block-class tasks get 8x the budget (8 warps share one table)
-            const int64_t ch = task_class(dv, force) == 2 ? chunk * kWarps : chunk;
+            const int64_t ch = head_class(dag_ptr, dag_col, v, force, bm_bits) == 2 ? chunk * kWarps : chunk;
             if (i == s) f = 1;
             else if (pref[i] / ch != pref[i - 1] / ch) f = 1;
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
@@ -93,14 +108,15 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
 
 __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int64_t m,
                             const int32_t* __restrict__ in_dst, const int64_t* __restrict__ in_ptr,
-                            const int64_t* __restrict__ dag_ptr, int force, uint32_t* __restrict__ cls,
-                            uint64_t* __restrict__ packed, unsigned long long* __restrict__ hist) {
+                            const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col, int force,
+                            uint32_t bm_bits, uint32_t* __restrict__ cls, uint64_t* __restrict__ packed,
+                            unsigned long long* __restrict__ hist) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ntask; j += (int64_t)gridDim.x * blockDim.x) {
         int i0 = sel[j];
         int v = in_dst[i0];
         int64_t nxt = (j + 1 < ntask) ? (int64_t)sel[j + 1] : m;
         int64_t i1 = min(nxt, in_ptr[v + 1]);
-        int k = task_class(dag_ptr[v + 1] - dag_ptr[v], force);
+        int k = head_class(dag_ptr, dag_col, v, force, bm_bits);
         cls[j] = (uint32_t)k;
         packed[j] = (uint64_t)(uint32_t)i0 | ((uint64_t)(uint32_t)i1 << 32);
         atomicAdd(hist + k, 1ULL);
@@ -151,22 +167,27 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             const int b = __shfl_sync(0xffffffffu, beg, s);
             const int e = b + __shfl_sync(0xffffffffu, len, s);
             uint32_t seg_hits = 0;
-            for (int q0 = (b & ~3) + lane * 4; q0 < e; q0 += 128) {
-                const int4 w4 = __ldg(reinterpret_cast<const int4*>(dag_col + q0));
-                const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int q = q0 + k;
-                    if (q >= b && q < e) {
-                        const int slot = probe.find((uint32_t)wv[k]);
-                        if (slot >= 0) {
-                            ++seg_hits;
-                            if (SUP) {
-                                probe.credit(slot, sup);       // role (v,w)
-                                atomicAdd(sup + q, 1u);        // role (u,w)
-                            }
+            auto visit = [&](int q, int w) {
+                if (q >= b && q < e) {
+                    const int slot = probe.find((uint32_t)w);
+                    if (slot >= 0) {
+                        ++seg_hits;
+                        if (SUP) {
+                            probe.credit(slot, sup);       // role (v,w)
+                            atomicAdd(sup + q, 1u);        // role (u,w)
                         }
                     }
+                }
+            };
+            // two 16-byte loads in flight per lane (256 wedges per warp step)
+            for (int q0 = (b & ~3) + lane * 4; q0 < e; q0 += 256) {
+                const int4 A = __ldg(reinterpret_cast<const int4*>(dag_col + q0));
+                const bool two = q0 + 128 < e;
+                int4 B = make_int4(0, 0, 0, 0);
+                if (two) B = __ldg(reinterpret_cast<const int4*>(dag_col + q0 + 128));
+                visit(q0, A.x); visit(q0 + 1, A.y); visit(q0 + 2, A.z); visit(q0 + 3, A.w);
+                if (two) {
+                    visit(q0 + 128, B.x); visit(q0 + 129, B.y); visit(q0 + 130, B.z); visit(q0 + 131, B.w);
                 }
             }
             hits += seg_hits;
@@ -263,6 +284,7 @@ struct KArgs {
     int* next;                  // dynamic task counter
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
     int long_seg;               // suffix length threshold of the warp-vector path
+    int batch;                  // heavy-head kernel: consecutive tasks per batch
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -331,7 +353,6 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
 // probe, no probe chains), else as the 8192-slot hash.  The task's wedges
 // are split exactly into 8 equal cost-unit slices, one per warp, so the
 // block barrier after the stream does not wait on a straggler warp.
-constexpr int kBW = 16384;   // bitmap words (64 KB): 524288 ranks
 
 template <bool SUP>
 struct SmemBitmap {
@@ -388,46 +409,83 @@ __global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
     constexpr int max_lg = __builtin_ctz(kTS2);
     static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
     uint32_t hits = 0;
-    for (int64_t t = blockIdx.x; t < a.ntask; t += gridDim.x) {
+    // Tasks are dealt to blocks in batches of a.batch consecutive tasks,
+    // round-robin, so all blocks advance through the heads in rank order
+    // together (adjacent hubs share in-neighbours, whose rows then hit in L2)
+    // while consecutive tasks of one head share its table: the block
+    // synchronises only when the head changes.  Invariant: the bitmap region
+    // is all zero between heads.
+    const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
+    for (int j = threadIdx.x; j < kBW; j += blockDim.x) bits[j] = 0u;
+    int cur = -1, d = 0, lg = 0, ts = 0;
+    int64_t r0 = 0;
+    uint32_t span = 0;
+    bool use_bm = false;
+    auto teardown = [&](bool clear) {
+        if (SUP) {
+            if (use_bm) {
+                for (int j = threadIdx.x; j < d; j += blockDim.x)
+                    if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
+            } else {
+                for (int j = threadIdx.x; j < ts; j += blockDim.x)
+                    if (hcnt[j]) atomicAdd(a.sup + r0 + vals[j], hcnt[j]);
+            }
+        }
+        if (clear) {
+            if (use_bm) {
+                for (int j = threadIdx.x; j < d; j += blockDim.x)
+                    bits[((uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)cur - 1u) >> 5] = 0u;
+            } else {
+                for (int j = threadIdx.x; j < ts; j += blockDim.x) {
+                    keys[j] = 0u;
+                    vals[j] = 0;
+                }
+            }
+        }
+    };
+    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x)
+    for (int64_t t = bt * a.batch; t < min(a.ntask, (bt + 1) * a.batch); ++t) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
         if (!owned(a, i0)) continue;
         const int v = __ldg(a.in_dst + i0);
-        const int64_t r0 = __ldg(a.dag_ptr + v);
-        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
-        const uint32_t span = (uint32_t)__ldg(a.dag_col + r0 + d - 1) - (uint32_t)v;   // max rank - v
-        const bool use_bm = span <= a.bm_bits;
-        int lg = 0, ts = 0;
-        if (use_bm) {
-            const int nwords = (int)((span + 31) >> 5);
-            for (int j = threadIdx.x; j < nwords; j += blockDim.x) bits[j] = 0u;
-            if (SUP)
-                for (int j = threadIdx.x; j < d; j += blockDim.x) bcnt[j] = 0u;
+        if (v != cur) {
+            __syncthreads();                      // every warp is done with cur's table
+            if (cur >= 0) teardown(true);
             __syncthreads();
-            for (int j = threadIdx.x; j < d; j += blockDim.x) {
-                const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
-                atomicOr(bits + (x >> 5), 1u << (x & 31));
-                if (SUP) {
-                    const bool first = j == 0 || (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 5) != (x >> 5);
-                    if (first) pre[x >> 5] = (uint16_t)j;
+            cur = v;
+            r0 = __ldg(a.dag_ptr + v);
+            d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
+            span = (uint32_t)__ldg(a.dag_col + r0 + d - 1) - (uint32_t)v;   // max rank - v
+            use_bm = span <= a.bm_bits;
+            if (use_bm) {
+                for (int j = threadIdx.x; j < d; j += blockDim.x) {
+                    if (SUP) bcnt[j] = 0u;
+                    const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
+                    atomicOr(bits + (x >> 5), 1u << (x & 31));
+                    if (SUP) {
+                        const bool first = j == 0 ||
+                            (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 5) != (x >> 5);
+                        if (first) pre[x >> 5] = (uint16_t)j;
+                    }
+                }
+            } else {
+                lg = table_lg(d, max_lg);
+                ts = 1 << lg;
+                for (int j = threadIdx.x; j < ts; j += blockDim.x) {
+                    keys[j] = kEmpty;
+                    if (SUP) hcnt[j] = 0;
+                }
+                __syncthreads();
+                for (int j = threadIdx.x; j < d; j += blockDim.x) {
+                    uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
+                    uint32_t h = hash_slot(w, lg);
+                    while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
+                    if (SUP) vals[h] = j;
                 }
             }
-        } else {
-            lg = table_lg(d, max_lg);
-            ts = 1 << lg;
-            for (int j = threadIdx.x; j < ts; j += blockDim.x) {
-                keys[j] = kEmpty;
-                if (SUP) hcnt[j] = 0;
-            }
             __syncthreads();
-            for (int j = threadIdx.x; j < d; j += blockDim.x) {
-                uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
-                uint32_t h = hash_slot(w, lg);
-                while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
-                if (SUP) vals[h] = j;
-            }
         }
-        __syncthreads();
         // this warp's eighth of the task's cost units
         const int64_t c0 = __ldg(a.in_cost + i0), c1 = __ldg(a.in_cost + i1);
         const int64_t ca = c0 + (c1 - c0) * warp / kWarps, cb = c0 + (c1 - c0) * (warp + 1) / kWarps;
@@ -444,18 +502,9 @@ __global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
                                                a.dag_col, a.sup, seg, H, lane, a.long_seg);
             }
         }
-        __syncthreads();
-        if (SUP) {
-            if (use_bm) {
-                for (int j = threadIdx.x; j < d; j += blockDim.x)
-                    if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
-            } else {
-                for (int j = threadIdx.x; j < ts; j += blockDim.x)
-                    if (hcnt[j]) atomicAdd(a.sup + r0 + vals[j], hcnt[j]);
-            }
-            __syncthreads();
-        }
     }
+    __syncthreads();
+    if (cur >= 0) teardown(false);
     add_count(a.count, hits, lane);
 }
 
@@ -516,6 +565,8 @@ int occupancy_grid(K kernel, size_t smem) {
 
 }  // namespace
 
+static uint32_t bm_bits_of(const gc_ctx* c) { return c->block_bitmap ? (uint32_t)kBW * 32u : 0u; }
+
 int prepare_tasks(gc_ctx* c) {
     const int64_t m = c->m;
     c->tasks_ready = false;
@@ -534,7 +585,7 @@ int prepare_tasks(gc_ctx* c) {
     GC_TRY(ensure(c, c->vals_a, (size_t)(m + 1) * 4));     // flags (uint8) / selected indices
     GC_TRY(ensure(c, c->vals_b, (size_t)(m + 1) * 4));
     GC_TRY(ensure(c, c->keys_a, (size_t)(m + 1) * 8));
-    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(ensure(c, c->scal, 1024));
     GC_TRY(host_scratch(c, 4096));
     int64_t* h = static_cast<int64_t*>(c->hpin);
     int64_t* cost = c->tmp_a.as<int64_t>();
@@ -555,8 +606,8 @@ int prepare_tasks(gc_ctx* c) {
     }
     uint8_t* flags = reinterpret_cast<uint8_t*>(c->vals_b.p);
     GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(),
-              c->in_ptr.as<int64_t>(), c->dag_ptr.as<int64_t>(), m, c->task_chunk, c->total_cost, c->task_parts,
-              c->force_class, flags);
+              c->in_ptr.as<int64_t>(), c->dag_ptr.as<int64_t>(), c->dag_col.as<int32_t>(), m, c->task_chunk,
+              c->total_cost, c->task_parts, c->force_class, bm_bits_of(c), flags);
     int32_t* sel = c->vals_a.as<int32_t>();
     int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 128);
     thrust::counting_iterator<int32_t> iota(0);
@@ -574,7 +625,8 @@ int prepare_tasks(gc_ctx* c) {
     uint32_t* cls = reinterpret_cast<uint32_t*>(c->keys_a.p);
     uint32_t* cls_sorted = cls + (m + 1);
     GC_LAUNCH(c, k_task_fill, grid_for(nt), kThreads, 0, sel, nt, m, c->in_dst.as<int32_t>(), c->in_ptr.as<int64_t>(),
-              c->dag_ptr.as<int64_t>(), c->force_class, cls, c->tmp_b.as<uint64_t>(), hist);
+              c->dag_ptr.as<int64_t>(), c->dag_col.as<int32_t>(), c->force_class, bm_bits_of(c), cls,
+              c->tmp_b.as<uint64_t>(), hist);
     tmp = 0;
     GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
                                                c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
@@ -614,8 +666,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.owner = owner;
     a.sup = sup;
     a.count = count;
-    a.bm_bits = c->block_bitmap ? (uint32_t)kBW * 32u : 0u;
+    a.bm_bits = bm_bits_of(c);
     a.long_seg = c->long_seg;
+    a.batch = c->block_batch;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
     // class 2 first (heaviest tasks), then 1, 0, 3
     if (c->ntask[2] > 0) {
@@ -681,7 +734,7 @@ static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
 }
 
 int triangle_count(gc_ctx* c, uint64_t* out) {
-    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(ensure(c, c->scal, 1024));
     GC_TRY(host_scratch(c, 4096));
     unsigned long long* count = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 192);
     GC_TRY(record(c, 2));
@@ -702,7 +755,7 @@ int triangle_count(gc_ctx* c, uint64_t* out) {
 int support_dag(gc_ctx* c) {
     const int64_t m = c->m;
     GC_TRY(ensure(c, c->sup, (size_t)m * 4));
-    GC_TRY(ensure(c, c->scal, 256));
+    GC_TRY(ensure(c, c->scal, 1024));
     unsigned long long* count = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 200);
     GC_CUDA(c, cudaMemsetAsync(c->sup.p, 0, (size_t)m * 4, c->stream));
     GC_CUDA(c, cudaMemsetAsync(count, 0, 8, c->stream));

@@ -35,6 +35,7 @@ GC_OPT_TASK_CHUNK = 2
 GC_OPT_TIMING = 3
 GC_OPT_BLOCK_BITMAP = 4
 GC_OPT_LONG_SEG = 5
+GC_OPT_BLOCK_BATCH = 6
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -54,6 +55,7 @@ class gc_stats(ctypes.Structure):
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("wedges", ctypes.c_int64),
         ("q_out", ctypes.c_int64), ("q_in", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
         ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),
+        ("aux", ctypes.c_int64 * 8),
     ]
 
 
@@ -252,6 +254,7 @@ class Context:
         self._check(self._L.gc_get_stats(self._h, ctypes.byref(s)))
         out = {name: getattr(s, name) for name, _ in gc_stats._fields_}
         out["tasks"] = list(out["tasks"])
+        out["aux"] = list(out["aux"])
         return out
 
     def reset_stats(self):
