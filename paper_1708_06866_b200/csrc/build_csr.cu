@@ -14,6 +14,7 @@
 //
 // Radix sorts are CUB's (library primitive); everything else is ours.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "gc_internal.cuh"
@@ -92,13 +93,22 @@ __global__ void k_split_keys(const uint64_t* __restrict__ keys, int64_t m, int b
     }
 }
 
-// CSR row pointers from a row-sorted COO row array: ptr[x] = first i with row[i] >= x.
-__global__ void k_rows_from_sorted(const int32_t* __restrict__ row, int64_t m, int64_t n, int64_t* __restrict__ ptr) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t prev = (i == 0) ? -1 : (int64_t)row[i - 1];
-        int64_t cur = (i == m) ? n : (int64_t)row[i];
-        for (int64_t x = prev + 1; x <= cur; ++x) ptr[x] = i;
+// CSR row pointers from a row-sorted COO row array, in three parallel steps
+// (no thread walks a gap of empty rows): each run of equal rows records its
+// bounds, the row lengths are formed, and an exclusive scan gives ptr.
+__global__ void k_run_bounds(const int32_t* __restrict__ row, int64_t m, int32_t* __restrict__ first,
+                             int32_t* __restrict__ last) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = row[i];
+        if (i == 0 || row[i - 1] != r) first[r] = (int32_t)i;
+        if (i == m - 1 || row[i + 1] != r) last[r] = (int32_t)(i + 1);
     }
+}
+
+__global__ void k_row_len(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int64_t n,
+                          int64_t* __restrict__ len) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n; x += (int64_t)gridDim.x * blockDim.x)
+        len[x] = (x < n) ? (int64_t)(last[x] - first[x]) : 0;
 }
 
 __global__ void k_in_keys(const int32_t* __restrict__ col, const int32_t* __restrict__ src, int64_t m, int b,
@@ -163,6 +173,26 @@ __global__ void k_unpack_canon(const uint64_t* __restrict__ canon, int64_t m, in
 
 // Sort keys (and optional int32 payload) on bits [0, nbits); results in
 // keys_out / vals_out.
+// ptr[x] = first i with row[i] >= x, for a row-sorted array of length m.
+// Scratch: keys_a (first/last, 8n bytes), keys_b (lengths, 8(n+1) bytes).
+static int csr_ptr_from_sorted(gc_ctx* c, const int32_t* row, int64_t m, int64_t n, int64_t* ptr) {
+    GC_TRY(ensure(c, c->keys_a, (size_t)(n + 1) * 8));
+    GC_TRY(ensure(c, c->keys_b, (size_t)(n + 1) * 8));
+    int32_t* first = reinterpret_cast<int32_t*>(c->keys_a.p);
+    int32_t* last = first + n;
+    int64_t* len = c->keys_b.as<int64_t>();
+    GC_CUDA(c, cudaMemsetAsync(first, 0, (size_t)n * 8, c->stream));
+    if (m > 0) GC_LAUNCH(c, k_run_bounds, grid_for(m), kThreads, 0, row, m, first, last);
+    GC_LAUNCH(c, k_row_len, grid_for(n + 1), kThreads, 0, first, last, n, len);
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, ptr, n + 1, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, len, ptr, n + 1, c->stream));
+    c->stats.lib_launches += 2;
+    return GC_OK;
+}
+
 static int radix_sort(gc_ctx* c, const uint64_t* kin, uint64_t* kout, const int32_t* vin, int32_t* vout, int64_t N,
                       int nbits) {
     if (N <= 0) return GC_OK;
@@ -276,8 +306,7 @@ int build_csr(gc_ctx* c) {
         GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->dag_col.as<int32_t>(),
                   c->dag_src.as<int32_t>());
     }
-    GC_LAUNCH(c, k_rows_from_sorted, grid_for(m + 1), kThreads, 0, c->dag_src.as<int32_t>(), m, n,
-              c->dag_ptr.as<int64_t>());
+    GC_TRY(csr_ptr_from_sorted(c, c->dag_src.as<int32_t>(), m, n, c->dag_ptr.as<int64_t>()));
     // in-lists: sort (head, tail) with the DAG position as payload
     if (m > 0) {
         GC_LAUNCH(c, k_in_keys, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), c->dag_src.as<int32_t>(), m, b,
@@ -287,8 +316,7 @@ int build_csr(gc_ctx* c) {
         GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->in_src.as<int32_t>(),
                   c->in_dst.as<int32_t>());
     }
-    GC_LAUNCH(c, k_rows_from_sorted, grid_for(m + 1), kThreads, 0, c->in_dst.as<int32_t>(), m, n,
-              c->in_ptr.as<int64_t>());
+    GC_TRY(csr_ptr_from_sorted(c, c->in_dst.as<int32_t>(), m, n, c->in_ptr.as<int64_t>()));
 
     // ---- work-model statistics (one reduction over vertices)
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 512);

@@ -41,6 +41,8 @@ constexpr int kOvh = 2;                     // per in-edge overhead in the cost 
 constexpr int kD0 = 32, kD1 = 256, kD2 = 4096;
 constexpr int kTS0 = 64, kTS1 = 512;
 constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB): ranks (v, v + 2^18]
+
+extern __shared__ uint32_t g_dsmem[];   // dynamic shared memory of every kernel here
 constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not fit
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
@@ -168,14 +170,15 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             const int e = b + __shfl_sync(0xffffffffu, len, s);
             uint32_t seg_hits = 0;
             auto visit = [&](int q, int w) {
-                if (q >= b && q < e) {
+                const uint32_t inr = (uint32_t)(q - b) < (uint32_t)(e - b);
+                if (!SUP) {
+                    seg_hits += inr & probe.hit((uint32_t)w);     // branch-free for the bitmap
+                } else if (inr) {
                     const int slot = probe.find((uint32_t)w);
                     if (slot >= 0) {
                         ++seg_hits;
-                        if (SUP) {
-                            probe.credit(slot, sup);       // role (v,w)
-                            atomicAdd(sup + q, 1u);        // role (u,w)
-                        }
+                        probe.credit(slot, sup);       // role (v,w)
+                        atomicAdd(sup + q, 1u);        // role (u,w)
                     }
                 }
             };
@@ -221,11 +224,13 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             if (t < tot) {
                 const int q = bs + (t - es);
                 const uint32_t w = (uint32_t)__ldg(dag_col + q);
-                const int slot = probe.find(w);
-                if (slot >= 0) {
-                    hit = true;
-                    ++hits;
-                    if (SUP) {
+                if (!SUP) {
+                    hits += probe.hit(w);
+                } else {
+                    const int slot = probe.find(w);
+                    if (slot >= 0) {
+                        hit = true;
+                        ++hits;
                         probe.credit(slot, sup);       // role (v,w)
                         atomicAdd(sup + q, 1u);        // role (u,w)
                     }
@@ -266,6 +271,7 @@ struct SmemHash {
     __device__ __forceinline__ void credit(int slot, uint32_t*) const {
         if (SUP) atomicAdd(cnt + slot, 1u);
     }
+    __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
 
 struct KArgs {
@@ -302,7 +308,7 @@ __device__ __forceinline__ void add_count(unsigned long long* count, uint32_t hi
 // ------------------------------------------------- warp-task kernel (0, 1) --
 template <int TS, bool SUP>
 __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
-    extern __shared__ uint32_t smem[];
+    uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int per_warp = SUP ? (3 * TS + 32) : TS;
     uint32_t* keys = smem + warp * per_warp;
@@ -356,11 +362,19 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
 
 template <bool SUP>
 struct SmemBitmap {
-    const uint32_t* bits;
+    const uint32_t* bits;    // == g_dsmem (word 0 of the dynamic shared memory)
     const uint16_t* pre;     // SUP: index in N+(v) of the first element of each word
     uint32_t* cnt;           // SUP: (v,w)-role credits per index j
     uint32_t base;           // v + 1
     uint32_t nbits;
+    // membership only, branch-free: one LDS from the shared window (no
+    // generic-pointer conversion), word index clamped when out of range
+    __device__ __forceinline__ uint32_t hit(uint32_t w) const {
+        const uint32_t x = w - base;
+        const bool in = x < nbits;
+        const uint32_t word = g_dsmem[in ? (x >> 5) : 0u];
+        return (uint32_t)in & ((word >> (x & 31)) & 1u);
+    }
     __device__ __forceinline__ int find(uint32_t w) const {
         const uint32_t x = w - base;
         if (x >= nbits) return -1;
@@ -395,7 +409,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ 
 
 template <bool SUP>
 __global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
-    extern __shared__ uint32_t smem[];
+    uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
     // SUP: [kBW, kBW + kBW/2) u16 prefix | hash cnt ; then kD2 bitmap-mode cnt ; then seg
@@ -522,6 +536,7 @@ struct GlobalProbe {
         return (lo < d && (uint32_t)__ldg(row + lo) == w) ? lo : -1;
     }
     __device__ __forceinline__ void credit(int j, uint32_t* sup) const { atomicAdd(sup + r0 + j, 1u); }
+    __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
 
 template <bool SUP>
