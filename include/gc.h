@@ -82,6 +82,18 @@ const char* gc_last_error(const gc_ctx* ctx);
 int gc_nccl_unique_id(void* id_out /* 128 bytes */);
 int gc_comm_init(gc_ctx* ctx, const void* nccl_unique_id, int nranks, int rank);
 
+/* Host-only (no GPU, no context): the 1D work partition every rank computes
+ * identically.  cost_prefix: len+1 int64 values, the
+ * exclusive prefix sum of non-negative per-item costs (cost_prefix[len] =
+ * total).  Item i belongs to owner min(nparts - 1,
+ * floor(cost_prefix[i] * nparts / total)) (trailing zero-cost items go to the
+ * last owner).
+ * bounds_out[r] = first item of owner r (nondecreasing), bounds_out[nparts] =
+ * len; owner r holds [bounds_out[r], bounds_out[r+1]).  The intersection
+ * kernels apply the same rule to their task list.  Errors: NULL pointers,
+ * len < 0, nparts < 1 -> GC_ERR_INVALID. */
+int gc_partition_bounds(const int64_t* cost_prefix, int64_t len, int nparts, int64_t* bounds_out);
+
 /* Testing aid for the partitioned path on ONE GPU: nparts virtual ranks run
  * one after another in this process and their partial results are combined
  * by device sums instead of NCCL.  Results must equal nparts = 1. */

@@ -213,6 +213,23 @@ int gc_comm_init(gc_ctx* c, const void* id, int nranks, int rank) {
     return nccl_init(c, id, nranks, rank);
 }
 
+int gc_partition_bounds(const int64_t* pref, int64_t len, int nparts, int64_t* bounds) {
+    if (!pref || !bounds || len < 0 || nparts < 1) return GC_ERR_INVALID;
+    const int64_t total = pref[len];
+    // owner(i) = floor(pref[i] * nparts / total) is nondecreasing in i
+    int64_t i = 0;
+    for (int r = 0; r < nparts; ++r) {
+        if (total <= 0) {
+            bounds[r] = r == 0 ? 0 : len;
+            continue;
+        }
+        while (i < len && (pref[i] * (int64_t)nparts) / total < r) ++i;
+        bounds[r] = i;
+    }
+    bounds[nparts] = len;
+    return GC_OK;
+}
+
 int gc_comm_init_loopback(gc_ctx* c, int nparts) {
     GC_TRY(check_ctx(c));
     if (nparts < 1 || nparts > 64) return fail(c, GC_ERR_INVALID, "gc_comm_init_loopback: nparts must be 1..64");

@@ -171,15 +171,11 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             uint32_t seg_hits = 0;
             auto visit = [&](int q, int w) {
                 const uint32_t inr = (uint32_t)(q - b) < (uint32_t)(e - b);
-                if (!SUP) {
-                    seg_hits += inr & probe.hit((uint32_t)w);     // branch-free for the bitmap
-                } else if (inr) {
-                    const int slot = probe.find((uint32_t)w);
-                    if (slot >= 0) {
-                        ++seg_hits;
-                        probe.credit(slot, sup);       // role (v,w)
-                        atomicAdd(sup + q, 1u);        // role (u,w)
-                    }
+                const uint32_t h = inr & probe.hit((uint32_t)w);  // branch-free for the bitmap
+                seg_hits += h;
+                if (SUP && h) {
+                    probe.credit(probe.find((uint32_t)w), sup);   // role (v,w)
+                    atomicAdd(sup + q, 1u);                       // role (u,w)
                 }
             };
             // two 16-byte loads in flight per lane (256 wedges per warp step)
@@ -408,7 +404,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ 
 }
 
 template <bool SUP>
-__global__ void __launch_bounds__(256) k_tc_block(KArgs a) {
+__global__ void __launch_bounds__(256, SUP ? 3 : 6) k_tc_block(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;

@@ -42,7 +42,7 @@ EXPORTS = [
     "gc_create", "gc_destroy", "gc_last_error", "gc_nccl_unique_id", "gc_comm_init",
     "gc_comm_init_loopback", "gc_load_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
     "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_truss_decomposition",
-    "gc_set_option", "gc_get_stats", "gc_reset_stats",
+    "gc_set_option", "gc_get_stats", "gc_reset_stats", "gc_partition_bounds",
 ]
 
 
@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "gc_set_option": ([_vp, ctypes.c_int, _i64], ctypes.c_int),
         "gc_get_stats": ([_vp, ctypes.POINTER(gc_stats)], ctypes.c_int),
         "gc_reset_stats": ([_vp], ctypes.c_int),
+        "gc_partition_bounds": ([_vp, _i64, ctypes.c_int, _vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -259,6 +260,17 @@ class Context:
 
     def reset_stats(self):
         self._check(self._L.gc_reset_stats(self._h))
+
+
+def partition_bounds(cost_prefix, nparts: int) -> np.ndarray:
+    """Host-side 1D owner cut (gc_partition_bounds): owner r holds [b[r], b[r+1])."""
+    pref = np.ascontiguousarray(cost_prefix, dtype=np.int64)
+    out = np.zeros(int(nparts) + 1, dtype=np.int64)
+    rc = load_library().gc_partition_bounds(_vp(pref.ctypes.data), pref.size - 1, int(nparts),
+                                             _vp(out.ctypes.data))
+    if rc != GC_OK:
+        raise GcError(rc, "gc_partition_bounds: bad arguments")
+    return out
 
 
 def init_distributed(ctx: Context, group=None):

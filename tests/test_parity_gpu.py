@@ -210,6 +210,42 @@ def test_c3_tc_support_and_ktruss(ctx):
         assert np.array_equal(ctx.edge_support(), g.support())
 
 
+def test_c4_full_size_sampled(gcmod):
+    """BASELINE configs[3] at full size, in bench.py's launch configuration
+    (torch's stream, device-resident inputs): supports of sampled edges are
+    recomputed one by one by the oracle; T = Σ support / 3; the 3-truss mask
+    is checked on sampled survivors (support inside the truss >= 1) and on
+    sampled removed edges (no triangle survives in the truss)."""
+    import torch
+    u, v = gen.CONFIGS["C4"].generate()
+    c = gcmod.Context(0, torch.cuda.current_stream())
+    try:
+        c.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+        c.build_csr()
+        m = c.num_edges()
+        T = c.triangle_count()
+        sup = c.edge_support()
+        cu, cv = c.get_edges()
+        mask, m_alive = c.ktruss(3)
+    finally:
+        c.close()
+    assert int(sup.astype(np.int64).sum()) == 3 * T
+    g = oracle.OracleGraph(u, v)
+    assert g.m == m
+    assert np.array_equal(cu, g.cu) and np.array_equal(cv, g.cv)
+    rng = np.random.default_rng(4)
+    idx = np.sort(rng.choice(m, size=20000, replace=False))
+    assert np.array_equal(sup[idx], g.support_pairs(g.cu[idx], g.cv[idx]))
+    # 3-truss: the survivors form a graph in which every sampled survivor has support >= 1,
+    # and every edge with zero support was removed
+    assert m_alive == int(mask.sum())
+    assert not np.any(mask[sup == 0])
+    keep = np.flatnonzero(mask)
+    h = oracle.OracleGraph(g.cu[keep], g.cv[keep])
+    sample = rng.choice(keep.size, size=min(20000, keep.size), replace=False)
+    assert np.all(h.support_pairs(g.cu[keep][sample], g.cv[keep][sample]) >= 1)
+
+
 # ------------------------------------------------------- kernel class forcing --
 @pytest.mark.parametrize("force", [0, 1, 2, 3])
 def test_forced_classes(ctx, gcmod, force):
