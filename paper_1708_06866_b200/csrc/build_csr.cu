@@ -111,12 +111,15 @@ __global__ void k_row_len(const int32_t* __restrict__ first, const int32_t* __re
         len[x] = (x < n) ? (int64_t)(last[x] - first[x]) : 0;
 }
 
-__global__ void k_in_keys(const int32_t* __restrict__ col, const int32_t* __restrict__ src, int64_t m, int b,
-                          uint64_t* __restrict__ ikeys, int32_t* __restrict__ iota) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
-        ikeys[p] = ((uint64_t)(uint32_t)col[p] << b) | (uint32_t)src[p];
-        iota[p] = (int32_t)p;
-    }
+__global__ void k_iota(int32_t* __restrict__ a, int64_t m) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
+        a[p] = (int32_t)p;
+}
+
+__global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t m,
+                             int32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = src[idx[i]];
 }
 
 // Work-model sums over vertices: wedges = Σ C(d+,2), Q_out = Σ d+², Q_in = Σ d- d+,
@@ -309,12 +312,21 @@ int build_csr(gc_ctx* c) {
     GC_TRY(csr_ptr_from_sorted(c, c->dag_src.as<int32_t>(), m, n, c->dag_ptr.as<int64_t>()));
     // in-lists: sort (head, tail) with the DAG position as payload
     if (m > 0) {
-        GC_LAUNCH(c, k_in_keys, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), c->dag_src.as<int32_t>(), m, b,
-                  c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
-        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
-                          c->in_pos.as<int32_t>(), m, 2 * b));
-        GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->in_src.as<int32_t>(),
-                  c->in_dst.as<int32_t>());
+        // DAG order is sorted by (tail, head): a stable sort on the head alone
+        // (b-bit keys, 32-bit) groups in-edges by head with tails ascending.
+        GC_LAUNCH(c, k_iota, grid_for(m), kThreads, 0, c->vals_a.as<int32_t>(), m);
+        size_t tmp = 0;
+        const uint32_t* hk = reinterpret_cast<const uint32_t*>(c->dag_col.p);
+        uint32_t* hk_out = reinterpret_cast<uint32_t*>(c->in_dst.p);
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, hk, hk_out, c->vals_a.as<int32_t>(),
+                                                   c->in_pos.as<int32_t>(), m, 0, b, c->stream));
+        GC_TRY(ensure(c, c->cub_tmp, tmp));
+        tmp = c->cub_tmp.cap;
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hk, hk_out, c->vals_a.as<int32_t>(),
+                                                   c->in_pos.as<int32_t>(), m, 0, b, c->stream));
+        c->stats.lib_launches += 2 + (b + 7) / 8;
+        GC_LAUNCH(c, k_gather_i32, grid_for(m), kThreads, 0, c->dag_src.as<int32_t>(), c->in_pos.as<int32_t>(), m,
+                  c->in_src.as<int32_t>());
     }
     GC_TRY(csr_ptr_from_sorted(c, c->in_dst.as<int32_t>(), m, n, c->in_ptr.as<int64_t>()));
 

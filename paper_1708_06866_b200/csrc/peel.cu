@@ -99,6 +99,12 @@ __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front,
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
         const int e = front[wi];
+        // S(e) is exact at round start (every destroyed triangle decremented its
+        // survivors) and frontier edges are not decremented in their own round:
+        // it is the number of live triangles through e.  None: nothing to do
+        // (the whole k = 3 peel); otherwise stop once all S(e) are found.
+        const uint32_t live = S[e];
+        if (live == 0) continue;
         const int a = dag_src[e], b = dag_col[e];
         int64_t a0 = sym_ptr[a], a1 = sym_ptr[a + 1], b0 = sym_ptr[b], b1 = sym_ptr[b + 1];
         // iterate the shorter row, search the longer
@@ -106,14 +112,24 @@ __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front,
             int64_t t0 = a0, t1 = a1;
             a0 = b0; a1 = b1; b0 = t0; b1 = t1;
         }
-        for (int64_t i = a0 + lane; i < a1; i += 32) {
-            const int f = __ldg(sym_eid + i);
-            if (f == e || !alive[f]) continue;
-            const int32_t w = __ldg(sym_col + i);
-            const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
-            if (j >= b1 || __ldg(sym_col + j) != w) continue;
-            const int g = __ldg(sym_eid + j);
-            if (!alive[g]) continue;
+        uint32_t found = 0;
+        for (int64_t base = a0; base < a1 && found < live; base += 32) {
+            const int64_t i = base + lane;
+            bool tri = false;
+            int f = -1, g = -1;
+            if (i < a1) {
+                f = __ldg(sym_eid + i);
+                if (f != e && alive[f]) {
+                    const int32_t w = __ldg(sym_col + i);
+                    const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
+                    if (j < b1 && __ldg(sym_col + j) == w) {
+                        g = __ldg(sym_eid + j);
+                        tri = alive[g] != 0;
+                    }
+                }
+            }
+            found += __popc(__ballot_sync(0xffffffffu, tri));
+            if (!tri) continue;
             const bool fx = rem[f] == round, gx = rem[g] == round;
             if ((fx && f < e) || (gx && g < e)) continue;   // a smaller X-edge owns this triangle
             if (!fx) {
