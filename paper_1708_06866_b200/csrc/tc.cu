@@ -40,7 +40,8 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kOvh = 2;                     // per in-edge overhead in the cost model
 constexpr int kD0 = 32, kD1 = 256, kD2 = 4096;
 constexpr int kTS0 = 64, kTS1 = 512;
-constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB): ranks (v, v + 2^18]
+constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB); the last one is a zero
+constexpr int kBWS = kBW;      // sentinel, so heads spanning <= 32*(kBW-1) ranks fit
 
 extern __shared__ uint32_t g_dsmem[];   // dynamic shared memory of every kernel here
 constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not fit
@@ -178,16 +179,23 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                     atomicAdd(sup + q, 1u);                       // role (u,w)
                 }
             };
+            // a vector wholly inside [b, e) needs no per-element bounds checks
+            auto visit4 = [&](int q0, const int4& V) {
+                if (!SUP && q0 >= b && q0 + 4 <= e) {
+                    seg_hits += probe.hit((uint32_t)V.x) + probe.hit((uint32_t)V.y) + probe.hit((uint32_t)V.z) +
+                                probe.hit((uint32_t)V.w);
+                } else {
+                    visit(q0, V.x); visit(q0 + 1, V.y); visit(q0 + 2, V.z); visit(q0 + 3, V.w);
+                }
+            };
             // two 16-byte loads in flight per lane (256 wedges per warp step)
             for (int q0 = (b & ~3) + lane * 4; q0 < e; q0 += 256) {
                 const int4 A = __ldg(reinterpret_cast<const int4*>(dag_col + q0));
                 const bool two = q0 + 128 < e;
                 int4 B = make_int4(0, 0, 0, 0);
                 if (two) B = __ldg(reinterpret_cast<const int4*>(dag_col + q0 + 128));
-                visit(q0, A.x); visit(q0 + 1, A.y); visit(q0 + 2, A.z); visit(q0 + 3, A.w);
-                if (two) {
-                    visit(q0 + 128, B.x); visit(q0 + 129, B.y); visit(q0 + 130, B.z); visit(q0 + 131, B.w);
-                }
+                visit4(q0, A);
+                if (two) visit4(q0 + 128, B);
             }
             hits += seg_hits;
             if (SUP) {
@@ -359,17 +367,18 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
 template <bool SUP>
 struct SmemBitmap {
     const uint32_t* bits;    // == g_dsmem (word 0 of the dynamic shared memory)
-    const uint16_t* pre;     // SUP: index in N+(v) of the first element of each word
+    const uint16_t* pre;     // SUP: index in N+(v) of the first element of each 64-bit chunk
     uint32_t* cnt;           // SUP: (v,w)-role credits per index j
     uint32_t base;           // v + 1
     uint32_t nbits;
     // membership only, branch-free: one LDS from the shared window (no
-    // generic-pointer conversion), word index clamped when out of range
+    // generic-pointer conversion).  Words past the head's span are zero and
+    // word kBW-1 is a permanent zero sentinel, so clamping the word index is
+    // the whole range check (w > v always, so x never wraps).
     __device__ __forceinline__ uint32_t hit(uint32_t w) const {
         const uint32_t x = w - base;
-        const bool in = x < nbits;
-        const uint32_t word = g_dsmem[in ? (x >> 5) : 0u];
-        return (uint32_t)in & ((word >> (x & 31)) & 1u);
+        const uint32_t word = g_dsmem[min(x >> 5, (uint32_t)(kBW - 1))];
+        return (word >> (x & 31)) & 1u;
     }
     __device__ __forceinline__ int find(uint32_t w) const {
         const uint32_t x = w - base;
@@ -378,7 +387,9 @@ struct SmemBitmap {
         const uint32_t bit = 1u << (x & 31);
         if (!(word & bit)) return -1;
         if (!SUP) return 0;
-        return (int)pre[x >> 5] + __popc(word & (bit - 1));
+        // pre holds the index of the first element of each 64-bit chunk
+        const uint32_t lo = (x & 32) ? bits[(x >> 5) - 1] : 0u;   // lower word of the chunk
+        return (int)pre[x >> 6] + __popc(lo) + __popc(word & (bit - 1));
     }
     __device__ __forceinline__ void credit(int j, uint32_t*) const {
         if (SUP) atomicAdd(cnt + j, 1u);
@@ -404,7 +415,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ 
 }
 
 template <bool SUP>
-__global__ void __launch_bounds__(256, SUP ? 3 : 6) k_tc_block(KArgs a) {
+__global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
@@ -412,10 +423,11 @@ __global__ void __launch_bounds__(256, SUP ? 3 : 6) k_tc_block(KArgs a) {
     uint32_t* bits = smem;
     uint32_t* keys = smem;
     int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
-    uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBW);
-    uint32_t* hcnt = smem + kBW;
-    uint32_t* bcnt = smem + kBW + kBW / 2;
-    uint32_t* seg = smem + (SUP ? kBW + kBW / 2 + kD2 : kBW) + warp * 32;
+    uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);    // kBW/2 u16 = kBW/4 words
+    uint32_t* hcnt = smem + kBWS;                                  // hash mode: kTS2 words
+    uint32_t* bcnt = smem + kBWS + kBW / 4;                        // bitmap mode: kD2 words
+    uint32_t* seg = nullptr;                                       // (unused: (u,v) credits use match_any)
+    static_assert(kTS2 <= kBW / 4 + kD2, "hash counters fit the SUP region");
     constexpr int max_lg = __builtin_ctz(kTS2);
     static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
     uint32_t hits = 0;
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(256, SUP ? 3 : 6) k_tc_block(KArgs a) {
     // synchronises only when the head changes.  Invariant: the bitmap region
     // is all zero between heads.
     const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
-    for (int j = threadIdx.x; j < kBW; j += blockDim.x) bits[j] = 0u;
+    for (int j = threadIdx.x; j < kBWS; j += blockDim.x) bits[j] = 0u;
     int cur = -1, d = 0, lg = 0, ts = 0;
     int64_t r0 = 0;
     uint32_t span = 0;
@@ -475,8 +487,8 @@ __global__ void __launch_bounds__(256, SUP ? 3 : 6) k_tc_block(KArgs a) {
                     atomicOr(bits + (x >> 5), 1u << (x & 31));
                     if (SUP) {
                         const bool first = j == 0 ||
-                            (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 5) != (x >> 5);
-                        if (first) pre[x >> 5] = (uint16_t)j;
+                            (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 6) != (x >> 6);
+                        if (first) pre[x >> 6] = (uint16_t)j;
                     }
                 }
             } else {
@@ -576,7 +588,7 @@ int occupancy_grid(K kernel, size_t smem) {
 
 }  // namespace
 
-static uint32_t bm_bits_of(const gc_ctx* c) { return c->block_bitmap ? (uint32_t)kBW * 32u : 0u; }
+static uint32_t bm_bits_of(const gc_ctx* c) { return c->block_bitmap ? (uint32_t)(kBW - 1) * 32u : 0u; }
 
 int prepare_tasks(gc_ctx* c) {
     const int64_t m = c->m;
@@ -686,7 +698,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         a.next = next + 2;
-        const size_t smem = (SUP ? kBW + kBW / 2 + kD2 + kWarps * 32 : kBW + kWarps * 32) * sizeof(uint32_t);
+        const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
             GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
