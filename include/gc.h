@@ -167,9 +167,16 @@ typedef enum gc_option {
     GC_OPT_LONG_SEG = 5,      /* suffixes at least this long take the warp-vector path
                                  (default 48; 2^30 disables it; testing) */
     GC_OPT_BLOCK_BATCH = 6,   /* heavy-head kernel: consecutive tasks per block batch,
-                                 batches dealt round-robin (default 4; tuning) */
+                                 batches dealt round-robin (default 32; tuning) */
     GC_OPT_BLOCK_BITMAP = 4,  /* 1: heavy-head kernel may use the rank-window bitmap
                                  (default); 0: always its hash table (testing) */
+    GC_OPT_SUP_UW = 7,        /* (u,w)-role support credits: 0 one global atomic per
+                                 triangle; 1 wedge hit-bitmap + per-row column sums;
+                                 99 skipped (timing diagnostics only: wrong supports) */
+    GC_OPT_PEEL_PART = 8,     /* 1: use the partitioned k-truss peeler (removed-edge
+                                 bitmap per round, owner-only decrements; the multi-GPU
+                                 path) even on a single rank (testing); it is always
+                                 used when nranks > 1 or under loopback partitions */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

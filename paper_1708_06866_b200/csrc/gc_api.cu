@@ -176,7 +176,7 @@ int gc_destroy(gc_ctx* c) {
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->rem, &c->front_a,
-                        &c->front_b, &c->tau, &c->bitmap};
+                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts};
     for (auto* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     nccl_destroy(c);
@@ -372,6 +372,13 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
                 GC_TRY(prepare_tasks(c));
                 GC_TRY(sync(c));
             }
+            return GC_OK;
+        case GC_OPT_SUP_UW:
+            if (value != 0 && value != 1 && value != 99) return fail(c, GC_ERR_INVALID, "sup_uw must be 0, 1 or 99");
+            c->sup_uw = (int)value;
+            return GC_OK;
+        case GC_OPT_PEEL_PART:
+            c->peel_part = value ? 1 : 0;
             return GC_OK;
         case GC_OPT_TIMING:
             c->timing = value ? 1 : 0;

@@ -60,6 +60,7 @@ struct gc_ctx {
     int block_bitmap = 1;
     int long_seg = 48;
     int block_batch = 32;
+    int sup_uw = 0;
 
     // raw input (a1)
     gcx::Buf raw_u, raw_v;
@@ -112,7 +113,10 @@ struct gc_ctx {
     gcx::Buf rem;       // int32[m] round in which the edge is in the frontier
     gcx::Buf front_a, front_b;  // int32[m] frontier lists
     gcx::Buf tau;       // int32[m]
-    gcx::Buf bitmap;    // uint32 removed-edge bitmap (multi-GPU exchange)
+    gcx::Buf xbits;     // uint32 removed-edge bitmap X of the round (partitioned peel, allgathered)
+    gcx::Buf nbits;     // uint32 next-round bitmap (each owner sets bits in its slice)
+    gcx::Buf sup_parts; // uint32[P*m] per-virtual-rank supports (loopback partitions only)
+    int peel_part = 0;  // 1: partitioned (bitmap) peeler even on one rank (GC_OPT_PEEL_PART)
 
     // pinned host scratch
     void* hpin = nullptr;

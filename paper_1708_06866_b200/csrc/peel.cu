@@ -21,6 +21,8 @@
 // until X is empty (fixed point).  Decomposition: k = 3, 4, ...
 // continue from the previous k's survivors; edges removed at level k get
 // trussness k-1.
+#include <algorithm>
+
 #include "gc_internal.cuh"
 
 namespace gcx {
@@ -150,6 +152,109 @@ __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front,
     }
 }
 
+// ---------------------------------------------- partitioned peel (§8(e) v1) --
+// Edges (DAG positions) are owned in word-aligned contiguous ranges, one per
+// rank; every rank keeps the replicated alive set and the exact support of
+// the edges it owns.  Per round the removed set X travels as a bitmap
+// (ncclAllGather of each owner's slice), every rank enumerates the destroyed
+// triangles of the whole X and decrements only the survivors it owns.
+
+// own slice of X at a level start: bit e = alive[e] && S[e] < thr, e in [lo, hi)
+__global__ void k_front_bits(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive, int64_t lo,
+                             int64_t hi, uint32_t thr, uint32_t* __restrict__ bits) {
+    // lo is a multiple of 32: thread e's ballot is word e / 32
+    for (int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < lo + (((hi - lo) + 31) & ~(int64_t)31);
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const bool in = e < hi && alive[e] && S[e] < thr;
+        const unsigned w = __ballot_sync(0xffffffffu, in);
+        if ((threadIdx.x & 31) == 0) bits[e >> 5] = w;
+    }
+}
+
+// list of the set bits of bits[0, nwords) (order unspecified)
+__global__ void k_bits_to_list(const uint32_t* __restrict__ bits, int64_t nwords, int32_t* __restrict__ list,
+                               int* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; w0 < nwords;
+         w0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = w0 + lane;
+        uint32_t x = w < nwords ? bits[w] : 0u;
+        const int c = __popc(x);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        int base = 0;
+        if (lane == 31 && tot) base = atomicAdd(count, tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            list[base++] = (int32_t)(w * 32 + b);
+        }
+    }
+}
+
+// k_peel with X given as a bitmap and decrements restricted to owned edges
+// [lo, hi); an owned survivor crossing thr -> thr-1 sets its bit in nbits.
+__global__ void __launch_bounds__(256) k_peel_part(const int32_t* __restrict__ front, int nfront,
+                                                   const int32_t* __restrict__ dag_src,
+                                                   const int32_t* __restrict__ dag_col,
+                                                   const int64_t* __restrict__ sym_ptr,
+                                                   const int32_t* __restrict__ sym_col,
+                                                   const int32_t* __restrict__ sym_eid,
+                                                   const uint8_t* __restrict__ alive, const uint32_t* __restrict__ xbits,
+                                                   uint32_t* __restrict__ S, uint32_t thr, int64_t lo, int64_t hi,
+                                                   uint32_t* __restrict__ nbits) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    auto in_x = [&](int f) { return (xbits[f >> 5] >> (f & 31)) & 1u; };
+    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
+        const int e = front[wi];
+        // S(e) is exact only when e is owned (an upper bound otherwise): it
+        // may end the search early only then.
+        const bool own_e = e >= lo && e < hi;
+        const uint32_t live = own_e ? S[e] : 0xFFFFFFFFu;
+        if (live == 0) continue;
+        const int a = dag_src[e], b = dag_col[e];
+        int64_t a0 = sym_ptr[a], a1 = sym_ptr[a + 1], b0 = sym_ptr[b], b1 = sym_ptr[b + 1];
+        if (a1 - a0 > b1 - b0) {
+            int64_t t0 = a0, t1 = a1;
+            a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+        }
+        uint32_t found = 0;
+        for (int64_t base = a0; base < a1 && found < live; base += 32) {
+            const int64_t i = base + lane;
+            bool tri = false;
+            int f = -1, g = -1;
+            if (i < a1) {
+                f = __ldg(sym_eid + i);
+                if (f != e && alive[f]) {
+                    const int32_t w = __ldg(sym_col + i);
+                    const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
+                    if (j < b1 && __ldg(sym_col + j) == w) {
+                        g = __ldg(sym_eid + j);
+                        tri = alive[g] != 0;
+                    }
+                }
+            }
+            found += __popc(__ballot_sync(0xffffffffu, tri));
+            if (!tri) continue;
+            const bool fx = in_x(f), gx = in_x(g);
+            if ((fx && f < e) || (gx && g < e)) continue;   // a smaller X-edge owns this triangle
+            if (!fx && f >= lo && f < hi) {
+                if (atomicSub(S + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
+            }
+            if (!gx && g >= lo && g < hi) {
+                if (atomicSub(S + g, 1u) == thr) atomicOr(nbits + (g >> 5), 1u << (g & 31));
+            }
+        }
+    }
+}
+
 __global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, uint8_t* __restrict__ alive,
                                int32_t* __restrict__ tau, int32_t level) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
@@ -228,6 +333,63 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     return GC_OK;
 }
 
+// ---- partitioned peel (multi-GPU v1; loopback virtual ranks on one GPU)
+static int peel_parts(const gc_ctx* c) {
+    if (c->nccl && c->nranks > 1) return c->nranks;
+    if (c->loop_parts > 1) return c->loop_parts;
+    return c->peel_part ? 1 : 0;   // 0: single-GPU frontier-list peeler
+}
+
+static int64_t part_words(const gc_ctx* c, int P) { return ((c->m + 31) / 32 + P - 1) / P; }
+
+static uint32_t* part_support(gc_ctx* c, int r) {
+    if (c->loop_parts > 1) return c->sup_parts.as<uint32_t>() + (size_t)r * c->m;
+    return c->sup.as<uint32_t>();
+}
+
+static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* removed) {
+    const int64_t m = c->m;
+    const int P = peel_parts(c);
+    const int64_t W = part_words(c, P);
+    const bool nccl = c->nccl && c->nranks > 1;
+    const int r_begin = nccl ? c->rank : 0, r_end = nccl ? c->rank + 1 : P;
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
+    int32_t* h = static_cast<int32_t*>(c->hpin);
+    uint32_t* xb = c->xbits.as<uint32_t>();
+    uint32_t* nb = c->nbits.as<uint32_t>();
+    int32_t* front = c->front_a.as<int32_t>();
+    *removed = 0;
+    auto lo_of = [&](int r) { return std::min<int64_t>(m, (int64_t)r * W * 32); };
+    auto hi_of = [&](int r) { return std::min<int64_t>(m, (int64_t)(r + 1) * W * 32); };
+    // X at the level start: each owner scans its range
+    GC_CUDA(c, cudaMemsetAsync(xb, 0, (size_t)P * W * 4, c->stream));
+    for (int r = r_begin; r < r_end; ++r)
+        if (hi_of(r) > lo_of(r))
+            GC_LAUNCH(c, k_front_bits, grid_for(hi_of(r) - lo_of(r)), kThreads, 0, part_support(c, r),
+                      c->alive.as<uint8_t>(), lo_of(r), hi_of(r), thr, xb);
+    for (;;) {
+        if (nccl) GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
+        GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, front, cnt);
+        GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(sync(c));
+        const int nf = h[0];
+        if (nf == 0) break;
+        GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
+        const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
+        for (int r = r_begin; r < r_end; ++r)
+            GC_LAUNCH(c, k_peel_part, blocks, 256, 0, front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                      c->sym_ptr.as<int64_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
+                      c->alive.as<uint8_t>(), xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb);
+        GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, front, nf, c->alive.as<uint8_t>(),
+                  level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
+        *removed += nf;
+        c->stats.peel_rounds++;
+        std::swap(xb, nb);
+    }
+    return GC_OK;
+}
+
 static int peel_setup(gc_ctx* c) {
     const int64_t m = c->m;
     GC_TRY(build_sym(c));
@@ -242,7 +404,25 @@ static int peel_setup(gc_ctx* c) {
         GC_LAUNCH(c, k_fill_i32, grid_for(m), kThreads, 0, c->rem.as<int32_t>(), m, (int32_t)-1);
     }
     c->stats.peel_rounds = 0;
+    const int P = peel_parts(c);
+    if (P > 0) {
+        const int64_t W = part_words(c, P);
+        GC_TRY(ensure(c, c->xbits, (size_t)P * W * 4));
+        GC_TRY(ensure(c, c->nbits, (size_t)P * W * 4));
+        if (c->loop_parts > 1 && m > 0) {
+            // every virtual rank starts from the combined exact support
+            GC_TRY(ensure(c, c->sup_parts, (size_t)P * m * 4));
+            for (int r = 0; r < P; ++r)
+                GC_CUDA(c, cudaMemcpyAsync(c->sup_parts.as<uint32_t>() + (size_t)r * m, c->sup.p, (size_t)m * 4,
+                                           cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
     return GC_OK;
+}
+
+static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed) {
+    if (peel_parts(c) > 0) return peel_level_part(c, thr, level, removed);
+    return peel_level(c, thr, level, round, removed);
 }
 
 int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
@@ -254,7 +434,7 @@ int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
     int64_t removed = 0;
     if (m > 0 && k > 2) {
         int32_t round = 0;
-        GC_TRY(peel_level(c, (uint32_t)(k - 2), -1, &round, &removed));
+        GC_TRY(peel_any(c, (uint32_t)(k - 2), -1, &round, &removed));
     }
     GC_TRY(ensure(c, c->out_tmp, (size_t)m));
     if (m > 0)
@@ -282,7 +462,7 @@ int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
     int32_t round = 0;
     for (int32_t k = 3; left > 0; ++k) {
         int64_t removed = 0;
-        GC_TRY(peel_level(c, (uint32_t)(k - 2), k - 1, &round, &removed));
+        GC_TRY(peel_any(c, (uint32_t)(k - 2), k - 1, &round, &removed));
         if (removed > 0) last = k - 1;
         left -= removed;
     }

@@ -141,7 +141,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                                                 const int64_t* __restrict__ in_cost,
                                                 const int64_t* __restrict__ dag_ptr,
                                                 const int32_t* __restrict__ dag_col, uint32_t* __restrict__ sup,
-                                                uint32_t* seg_cnt, Probe& probe, int lane, int long_seg) {
+                                                uint32_t* seg_cnt, Probe& probe, int lane, int long_seg, int uw) {
     uint32_t hits = 0;
     for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
@@ -176,7 +176,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                 seg_hits += h;
                 if (SUP && h) {
                     probe.credit(probe.find((uint32_t)w), sup);   // role (v,w)
-                    atomicAdd(sup + q, 1u);                       // role (u,w)
+                    if (uw == 0) atomicAdd(sup + q, 1u);          // role (u,w)
                 }
             };
             // a vector wholly inside [b, e) needs no per-element bounds checks
@@ -236,7 +236,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                         hit = true;
                         ++hits;
                         probe.credit(slot, sup);       // role (v,w)
-                        atomicAdd(sup + q, 1u);        // role (u,w)
+                        if (uw == 0) atomicAdd(sup + q, 1u);   // role (u,w)
                     }
                 }
             }
@@ -295,6 +295,7 @@ struct KArgs {
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
     int long_seg;               // suffix length threshold of the warp-vector path
     int batch;                  // heavy-head kernel: consecutive tasks per batch
+    int uw;                     // (u,w)-role crediting mode (GC_OPT_SUP_UW)
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
         __syncwarp();
         SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
         hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
-                                        seg, H, lane, a.long_seg);
+                                        seg, H, lane, a.long_seg, a.uw);
         if (SUP) {
             __syncwarp();
             for (int j = lane; j < ts; j += 32)
@@ -517,11 +518,11 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
             if (use_bm) {
                 SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u, span};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, seg, B, lane, a.long_seg);
+                                               a.dag_col, a.sup, seg, B, lane, a.long_seg, a.uw);
             } else {
                 SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, seg, H, lane, a.long_seg);
+                                               a.dag_col, a.sup, seg, H, lane, a.long_seg, a.uw);
             }
         }
     }
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(256) k_tc_search(KArgs a) {
         const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
         GlobalProbe G{a.dag_col + r0, d, r0};
         hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
-                                        segs + warp * 32, G, lane, a.long_seg);
+                                        segs + warp * 32, G, lane, a.long_seg, a.uw);
     }
     add_count(a.count, hits, lane);
 }
@@ -692,6 +693,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.bm_bits = bm_bits_of(c);
     a.long_seg = c->long_seg;
     a.batch = c->block_batch;
+    a.uw = c->sup_uw;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
     // class 2 first (heaviest tasks), then 1, 0, 3
     if (c->ntask[2] > 0) {

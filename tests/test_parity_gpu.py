@@ -317,8 +317,40 @@ def test_loopback_partitions(gcmod, parts):
         c.build_csr()
         assert c.triangle_count() == g.triangle_count()
         assert np.array_equal(c.edge_support(), g.support())
-        want, _ = g.ktruss(5)
-        assert np.array_equal(c.ktruss(5)[0], want)
+        for k in (3, 5, 7):
+            want, _ = g.ktruss(k)
+            assert np.array_equal(c.ktruss(k)[0], want), k
+        tau, kmax = c.truss_decomposition()
+        want_tau, want_kmax = g.truss_decomposition()
+        assert np.array_equal(tau, want_tau) and kmax == want_kmax
+
+
+@pytest.mark.parametrize("parts", [1, 2, 5])
+def test_partitioned_peeler_c1_and_fixtures(gcmod, parts):
+    """The multi-GPU peeler (removed-edge bitmap per round, owner-only
+    decrements): P = 1 through GC_OPT_PEEL_PART, P > 1 as
+    loopback virtual ranks with one support copy each.  Includes the A5
+    tie-break fixture, whose two simultaneous removals share a triangle."""
+    cases = [gen.CONFIGS["C1"].generate()]
+    d = json.load(open(os.path.join(GOLDEN, "k4_ear.json")))
+    cases.append((np.array(d["raw_u"], np.int32), np.array(d["raw_v"], np.int32)))
+    cases.append(random_graph(90, 0.3, np.random.default_rng(parts)))
+    for u, v in cases:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            if parts == 1:
+                c.set_option(gcmod.GC_OPT_PEEL_PART, 1)
+            else:
+                c.comm_init_loopback(parts)
+            c.load_edges(u, v)
+            c.build_csr()
+            for k in (3, 4, 6):
+                want, _ = g.ktruss(k)
+                mask, m_alive = c.ktruss(k)
+                assert np.array_equal(mask, want) and m_alive == int(want.sum()), k
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax = g.truss_decomposition()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
 # --------------------------------------------------- API / pointer kinds ----
