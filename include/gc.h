@@ -177,6 +177,9 @@ typedef enum gc_option {
                                  bitmap per round, owner-only decrements; the multi-GPU
                                  path) even on a single rank (testing); it is always
                                  used when nranks > 1 or under loopback partitions */
+    GC_OPT_HUGE_MAX = 9,      /* class-3 heads with d+ above this (default 8192, the
+                                 16384-slot shared hash at load 1/2) search N+(v) in
+                                 global memory instead (0..8192; testing) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

@@ -377,6 +377,10 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
             if (value != 0 && value != 1 && value != 99) return fail(c, GC_ERR_INVALID, "sup_uw must be 0, 1 or 99");
             c->sup_uw = (int)value;
             return GC_OK;
+        case GC_OPT_HUGE_MAX:
+            if (value < 0 || value > 8192) return fail(c, GC_ERR_INVALID, "huge-head hash limit must be 0..8192");
+            c->huge_max = (int)value;
+            return GC_OK;
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;
             return GC_OK;

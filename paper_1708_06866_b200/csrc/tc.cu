@@ -45,12 +45,15 @@ constexpr int kBWS = kBW;      // sentinel, so heads spanning <= 32*(kBW-1) rank
 
 extern __shared__ uint32_t g_dsmem[];   // dynamic shared memory of every kernel here
 constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not fit
+constexpr int kTS3 = 16384;    // huge-head hash slots (d+ <= kTS3/2 by default)
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
 // tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
-// d+ <= kD2H), 3 global binary search.  force raises the class (testing).
+// d+ <= kD2H), 3 block tasks on a 16384-slot shared hash (one or two blocks
+// per SM; d+ above the huge-hash limit searches N+(v) in global memory).
+// force raises the class (testing).
 __device__ __forceinline__ int head_class(const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col,
                                           int v, int force, uint32_t bm_bits) {
     const int64_t r0 = dag_ptr[v];
@@ -100,7 +103,7 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
         uint8_t f = 0;
         if (dv > 0 && pref[e] > pref[s]) {
             // block-class tasks get 8x the budget (8 warps share one table)
-            const int64_t ch = head_class(dag_ptr, dag_col, v, force, bm_bits) == 2 ? chunk * kWarps : chunk;
+            const int64_t ch = head_class(dag_ptr, dag_col, v, force, bm_bits) >= 2 ? chunk * kWarps : chunk;
             if (i == s) f = 1;
             else if (pref[i] / ch != pref[i - 1] / ch) f = 1;
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
@@ -296,6 +299,7 @@ struct KArgs {
     int long_seg;               // suffix length threshold of the warp-vector path
     int batch;                  // heavy-head kernel: consecutive tasks per batch
     int uw;                     // (u,w)-role crediting mode (GC_OPT_SUP_UW)
+    int huge_max;               // class 3: largest d+ held in the shared hash
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -415,21 +419,41 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ 
     return lo + __popc(__ballot_sync(0xffffffffu, less));
 }
 
-template <bool SUP>
-__global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
+// Probe of N+(v) in global memory (binary search): huge heads past the table.
+struct GlobalProbe {
+    const int32_t* row;
+    int d;
+    int64_t r0;
+    __device__ __forceinline__ int find(uint32_t w) const {
+        int lo = 0, hi = d;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if ((uint32_t)__ldg(row + mid) < w) lo = mid + 1; else hi = mid;
+        }
+        return (lo < d && (uint32_t)__ldg(row + lo) == w) ? lo : -1;
+    }
+    __device__ __forceinline__ void credit(int j, uint32_t* sup) const { atomicAdd(sup + r0 + j, 1u); }
+    __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
+};
+
+template <bool SUP, bool HUGE>
+__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
     // SUP: [kBW, kBW + kBW/2) u16 prefix | hash cnt ; then kD2 bitmap-mode cnt ; then seg
+    // HUGE (class 3): [0, kTS3) keys | [kTS3, 2 kTS3) vals | [2 kTS3, 3 kTS3) cnt (SUP only)
+    constexpr int kTSH = HUGE ? kTS3 : kTS2;
+    constexpr int kZero = HUGE ? kTS3 : kBWS;    // words kept zero between heads
     uint32_t* bits = smem;
     uint32_t* keys = smem;
-    int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
+    int32_t* vals = reinterpret_cast<int32_t*>(smem + kTSH);
     uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);    // kBW/2 u16 = kBW/4 words
-    uint32_t* hcnt = smem + kBWS;                                  // hash mode: kTS2 words
+    uint32_t* hcnt = HUGE ? smem + 2 * kTS3 : smem + kBWS;        // hash mode: kTSH words
     uint32_t* bcnt = smem + kBWS + kBW / 4;                        // bitmap mode: kD2 words
     uint32_t* seg = nullptr;                                       // (unused: (u,v) credits use match_any)
     static_assert(kTS2 <= kBW / 4 + kD2, "hash counters fit the SUP region");
-    constexpr int max_lg = __builtin_ctz(kTS2);
+    constexpr int max_lg = __builtin_ctz(kTSH);
     static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
     uint32_t hits = 0;
     // Tasks are dealt to blocks in batches of a.batch consecutive tasks,
@@ -439,13 +463,13 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
     // synchronises only when the head changes.  Invariant: the bitmap region
     // is all zero between heads.
     const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
-    for (int j = threadIdx.x; j < kBWS; j += blockDim.x) bits[j] = 0u;
+    for (int j = threadIdx.x; j < kZero; j += blockDim.x) bits[j] = 0u;
     int cur = -1, d = 0, lg = 0, ts = 0;
     int64_t r0 = 0;
     uint32_t span = 0;
-    bool use_bm = false;
+    bool use_bm = false, use_gp = false;   // use_gp: N+(v) too large for the table, search it in global memory
     auto teardown = [&](bool clear) {
-        if (SUP) {
+        if (SUP && !use_gp) {
             if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x)
                     if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
@@ -454,14 +478,14 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
                     if (hcnt[j]) atomicAdd(a.sup + r0 + vals[j], hcnt[j]);
             }
         }
-        if (clear) {
+        if (clear && !use_gp) {
             if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x)
                     bits[((uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)cur - 1u) >> 5] = 0u;
             } else {
                 for (int j = threadIdx.x; j < ts; j += blockDim.x) {
                     keys[j] = 0u;
-                    vals[j] = 0;
+                    if (!HUGE) vals[j] = 0;   // shares the bitmap region (kept zero); HUGE TC has no vals
                 }
             }
         }
@@ -480,8 +504,11 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
             r0 = __ldg(a.dag_ptr + v);
             d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
             span = (uint32_t)__ldg(a.dag_col + r0 + d - 1) - (uint32_t)v;   // max rank - v
-            use_bm = span <= a.bm_bits;
-            if (use_bm) {
+            use_bm = !HUGE && span <= a.bm_bits;
+            use_gp = HUGE && d > a.huge_max;
+            if (use_gp) {
+                // nothing to stage
+            } else if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x) {
                     if (SUP) bcnt[j] = 0u;
                     const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
@@ -515,7 +542,11 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
         if (cb > ca) {
             const int first = (int)warp_lower_bound(a.in_cost, i0, i1, ca + 1, lane) - 1;
             const int end = (int)warp_lower_bound(a.in_cost, i0, i1, cb, lane);
-            if (use_bm) {
+            if (use_gp) {
+                GlobalProbe G{a.dag_col + r0, d, r0};
+                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                                               a.dag_col, a.sup, seg, G, lane, a.long_seg, a.uw);
+            } else if (use_bm) {
                 SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u, span};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, seg, B, lane, a.long_seg, a.uw);
@@ -528,43 +559,6 @@ __global__ void __launch_bounds__(256, SUP ? 4 : 6) k_tc_block(KArgs a) {
     }
     __syncthreads();
     if (cur >= 0) teardown(false);
-    add_count(a.count, hits, lane);
-}
-
-// ------------------------------------------ binary-search kernel (3) --
-struct GlobalProbe {
-    const int32_t* row;
-    int d;
-    int64_t r0;
-    __device__ __forceinline__ int find(uint32_t w) const {
-        int lo = 0, hi = d;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if ((uint32_t)__ldg(row + mid) < w) lo = mid + 1; else hi = mid;
-        }
-        return (lo < d && (uint32_t)__ldg(row + lo) == w) ? lo : -1;
-    }
-    __device__ __forceinline__ void credit(int j, uint32_t* sup) const { atomicAdd(sup + r0 + j, 1u); }
-    __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
-};
-
-template <bool SUP>
-__global__ void __launch_bounds__(256) k_tc_search(KArgs a) {
-    __shared__ uint32_t segs[kWarps * 32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t hits = 0;
-    const int64_t nw = (int64_t)gridDim.x * kWarps;
-    for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < a.ntask; t += nw) {
-        const uint64_t pk = a.tasks[t];
-        const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
-        if (!owned(a, i0)) continue;
-        const int v = __ldg(a.in_dst + i0);
-        const int64_t r0 = __ldg(a.dag_ptr + v);
-        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
-        GlobalProbe G{a.dag_col + r0, d, r0};
-        hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
-                                        segs + warp * 32, G, lane, a.long_seg, a.uw);
-    }
     add_count(a.count, hits, lane);
 }
 
@@ -694,8 +688,24 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.long_seg = c->long_seg;
     a.batch = c->block_batch;
     a.uw = c->sup_uw;
+    a.huge_max = c->huge_max;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
-    // class 2 first (heaviest tasks), then 1, 0, 3
+    // classes 3 and 2 first (heaviest tasks), then 1, 0
+    if (c->ntask[3] > 0) {
+        a.tasks = tasks + c->task_off[3];
+        a.ntask = c->ntask[3];
+        a.next = next + 3;
+        const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
+        static bool attr_set[2] = {false, false};
+        if (!attr_set[SUP]) {
+            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+            attr_set[SUP] = true;
+        }
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(k_tc_block<SUP, true>, smem);
+        GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
+    }
     if (c->ntask[2] > 0) {
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
@@ -703,12 +713,13 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
-            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
             attr_set[SUP] = true;
         }
         static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_block<SUP>, smem);
-        GC_LAUNCH(c, k_tc_block<SUP>, (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
+        if (!grid) grid = occupancy_grid(k_tc_block<SUP, false>, smem);
+        GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
     }
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
@@ -733,14 +744,6 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         static int grid = 0;
         if (!grid) grid = occupancy_grid(k_tc_warp<kTS0, SUP>, smem);
         GC_LAUNCH(c, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
-    }
-    if (c->ntask[3] > 0) {
-        a.tasks = tasks + c->task_off[3];
-        a.ntask = c->ntask[3];
-        a.next = next + 3;
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_search<SUP>, 0);
-        GC_LAUNCH(c, k_tc_search<SUP>, (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, 0, a);
     }
     return GC_OK;
 }

@@ -38,6 +38,7 @@ GC_OPT_LONG_SEG = 5
 GC_OPT_BLOCK_BATCH = 6
 GC_OPT_SUP_UW = 7
 GC_OPT_PEEL_PART = 8
+GC_OPT_HUGE_MAX = 9
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [

@@ -10,6 +10,8 @@ p.add_argument("--config", default="C3")
 p.add_argument("--ks", default="")
 p.add_argument("--part", type=int, default=0)
 p.add_argument("--loop", type=int, default=0)
+p.add_argument("--tc", type=int, default=0)
+p.add_argument("--no-decomp", action="store_true")
 a = p.parse_args()
 t0 = time.time()
 u, v = gen.CONFIGS[a.config].generate()
@@ -24,11 +26,22 @@ ctx.build_csr()
 m = ctx.num_edges()
 st = ctx.stats()
 print(f"n={ctx.num_vertices()} m={m} build {st['build_ms']:.1f} ms", flush=True)
+if a.tc:
+    for r in range(a.tc):
+        T = ctx.triangle_count()
+        sup = torch.empty(m, dtype=torch.int32, device="cuda")
+        ctx.edge_support(sup)
+        st = ctx.stats()
+        print(f"T={T} tc {st['tc_kernel_ms']:.1f} ms support {st['support_kernel_ms']:.1f} ms wedges={st['wedges']} "
+              f"maxdeg={st['max_degree']} max_out={st['max_out_degree']} tasks={list(st['tasks'])}", flush=True)
+    print(f"mem peak {torch.cuda.mem_get_info()}", flush=True)
 for k in [int(x) for x in a.ks.split(",") if x]:
     mask = torch.empty(m, dtype=torch.uint8, device="cuda")
     _, alive = ctx.ktruss(k, mask)
     st = ctx.stats()
     print(f"ktruss({k}): {alive} edges, {st['ktruss_ms']:.1f} ms (peel {st['peel_ms']:.1f} ms, {st['peel_rounds']} rounds)", flush=True)
+if a.no_decomp:
+    sys.exit(0)
 tau = torch.empty(m, dtype=torch.int32, device="cuda")
 t0 = time.time()
 _, kmax = ctx.truss_decomposition(tau)

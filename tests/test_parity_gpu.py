@@ -284,6 +284,29 @@ def test_heavy_head_bitmap_and_hash(ctx, gcmod, bitmap):
         ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
 
 
+@pytest.mark.parametrize("huge_max", [0, 40, 8192])
+def test_huge_head_hash_and_global_probe(ctx, gcmod, huge_max):
+    """The huge-head (class 3) block kernel forced on all heads: shared hash
+    (d+ <= huge_max) and global binary search (d+ > huge_max), with small and
+    default task chunks (several block tasks per head, exact wedge split)."""
+    u, v = gen.rmat(13, 16, seed=23)
+    g = oracle.OracleGraph(u, v)
+    try:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, 3)
+        ctx.set_option(gcmod.GC_OPT_HUGE_MAX, huge_max)
+        run_gpu(ctx, u, v)
+        for chunk in (4096, 57):
+            ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, chunk)
+            assert ctx.triangle_count() == g.triangle_count()
+            assert np.array_equal(ctx.edge_support(), g.support())
+            want, _ = g.ktruss(4)
+            assert np.array_equal(ctx.ktruss(4)[0], want)
+    finally:
+        ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
+        ctx.set_option(gcmod.GC_OPT_HUGE_MAX, 8192)
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+
+
 def test_task_chunk_sizes(ctx, gcmod):
     u, v = gen.rmat(12, 16, seed=13)
     g = oracle.OracleGraph(u, v)
@@ -298,7 +321,7 @@ def test_task_chunk_sizes(ctx, gcmod):
 
 
 def test_large_clique_all_classes(ctx):
-    """K_4200: out-degrees span every class including the >4096 binary-search one."""
+    """K_4200: out-degrees span every class including the > 4096 huge-head one."""
     n = 4200
     iu, ju = np.triu_indices(n, 1)
     run_gpu(ctx, iu.astype(np.int32), ju.astype(np.int32))
