@@ -180,6 +180,9 @@ typedef enum gc_option {
     GC_OPT_HUGE_MAX = 9,      /* class-3 heads with d+ above this (default 8192, the
                                  16384-slot shared hash at load 1/2) search N+(v) in
                                  global memory instead (0..8192; testing) */
+    GC_OPT_COMPACT = 10,      /* peeler: drop dead entries from the adjacency rows each
+                                 time the live edge count falls to 1/value of the last
+                                 compaction (default 2; 0 or 1: never; testing) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 
@@ -197,6 +200,7 @@ typedef struct gc_stats {
     int64_t launches;         /* libgc kernel launches since gc_reset_stats */
     int64_t lib_launches;     /* CUB (library) kernel launches, estimated, same window */
     int64_t peel_rounds;      /* rounds of the last peel (ktruss or decomposition) */
+    int64_t compactions;      /* dead-entry compactions of the last peel */
     int64_t n, m;
     int64_t wedges;           /* sum over vertices of C(d+(x), 2): intersection work */
     int64_t q_out;            /* sum d+(x)^2   (SURVEY §8(d) byte model) */

@@ -176,7 +176,7 @@ int gc_destroy(gc_ctx* c) {
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->rem, &c->front_a,
-                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts};
+                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist};
     for (auto* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     nccl_destroy(c);
@@ -380,6 +380,10 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
         case GC_OPT_HUGE_MAX:
             if (value < 0 || value > 8192) return fail(c, GC_ERR_INVALID, "huge-head hash limit must be 0..8192");
             c->huge_max = (int)value;
+            return GC_OK;
+        case GC_OPT_COMPACT:
+            if (value < 0 || value > 1024) return fail(c, GC_ERR_INVALID, "compaction divisor must be 0..1024");
+            c->compact_div = (int)value;
             return GC_OK;
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;

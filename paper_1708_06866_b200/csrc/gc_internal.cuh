@@ -110,6 +110,15 @@ struct gc_ctx {
     gcx::Buf sym_col;   // int32[2m]
     gcx::Buf sym_eid;   // int32[2m] DAG position of the edge
     bool sym_ready = false;
+    bool sym_dirty = true;  // rows were compacted (or never filled): refill before the next peel
+    gcx::Buf live_len;  // int32[n] live entries at the front of each symmetric row
+    gcx::Buf long_rows; // int32 rows longer than kLongRow (compacted block-wide)
+    int nlong = 0;
+    gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)
+    int64_t alist_n = -1;       // -1: no list (scan every edge)
+    int64_t m_alive_h = 0;      // live edges (host mirror)
+    int64_t compact_at = 0;     // live edges at the last compaction
+    int compact_div = 2;        // compact when live edges fall to 1/compact_div (GC_OPT_COMPACT; <= 1 never)
     gcx::Buf alive;     // uint8[m]
     gcx::Buf rem;       // int32[m] round in which the edge is in the frontier
     gcx::Buf front_a, front_b;  // int32[m] frontier lists

@@ -62,11 +62,125 @@ __global__ void k_fill_i32(int32_t* __restrict__ a, int64_t m, int32_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) a[i] = v;
 }
 
-// X = {alive e : S(e) < thr}
-__global__ void k_frontier_scan(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive, int64_t m,
-                                uint32_t thr, int32_t* __restrict__ rem, int32_t round, int32_t* __restrict__ front,
-                                int* __restrict__ count) {
+// ------------------------------------------------ dead-entry compaction --
+// As edges die, the symmetric rows fill with dead entries that every later
+// triangle search would still walk.  When the live edge count has halved
+// since the last compaction, each row's live entries are moved (stably, so
+// rows stay sorted) to the front of its own segment and live_len[x] records
+// the new length; the list of live edges is rebuilt for the level scans.
+__global__ void k_live_len_init(const int64_t* __restrict__ sym_ptr, int64_t n, int32_t* __restrict__ live_len) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        live_len[x] = (int32_t)(sym_ptr[x + 1] - sym_ptr[x]);
+}
+
+constexpr int kLongRow = 2048;   // rows longer than this are compacted by a whole block
+
+__global__ void k_long_rows(const int64_t* __restrict__ sym_ptr, int64_t n, int32_t* __restrict__ list,
+                            int* __restrict__ count) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        if (sym_ptr[x + 1] - sym_ptr[x] > kLongRow) list[atomicAdd(count, 1)] = (int32_t)x;
+}
+
+// one warp per row of at most kLongRow live entries; in place: each chunk of
+// 32 is read by the warp before any of it is written (writes never pass reads)
+__global__ void k_row_compact_warp(const int64_t* __restrict__ sym_ptr, int32_t* __restrict__ live_len,
+                                   int32_t* __restrict__ col, int32_t* __restrict__ eid,
+                                   const uint8_t* __restrict__ alive, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t x = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; x < n; x += nw) {
+        const int L = live_len[x];
+        if (L > kLongRow || L == 0) continue;
+        const int64_t base = sym_ptr[x];
+        int out = 0;
+        for (int i0 = 0; i0 < L; i0 += 32) {
+            const int i = i0 + lane;
+            int cv = 0, ev = 0;
+            bool keep = false;
+            if (i < L) {
+                cv = col[base + i];
+                ev = eid[base + i];
+                keep = alive[ev] != 0;
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) {
+                const int o = out + __popc(b & ((1u << lane) - 1));
+                col[base + o] = cv;
+                eid[base + o] = ev;
+            }
+            out += __popc(b);
+        }
+        if (lane == 0) live_len[x] = out;
+    }
+}
+
+// one block per long row (list built once with the symmetric CSR)
+__global__ void __launch_bounds__(256) k_row_compact_block(const int32_t* __restrict__ rows, int nrows,
+                                                            const int64_t* __restrict__ sym_ptr,
+                                                            int32_t* __restrict__ live_len, int32_t* __restrict__ col,
+                                                            int32_t* __restrict__ eid,
+                                                            const uint8_t* __restrict__ alive) {
+    __shared__ int wsum[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int x = rows[r];
+        const int L = live_len[x];
+        if (L <= kLongRow) continue;            // uniform per block
+        const int64_t base = sym_ptr[x];
+        int out = 0;
+        for (int i0 = 0; i0 < L; i0 += 256) {
+            const int i = i0 + threadIdx.x;
+            int cv = 0, ev = 0;
+            bool keep = false;
+            if (i < L) {
+                cv = col[base + i];
+                ev = eid[base + i];
+                keep = alive[ev] != 0;
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) wsum[warp] = __popc(b);
+            __syncthreads();
+            int before = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                before += w < warp ? wsum[w] : 0;
+                tot += wsum[w];
+            }
+            if (keep) {
+                const int o = out + before + __popc(b & ((1u << lane) - 1));
+                col[base + o] = cv;
+                eid[base + o] = ev;
+            }
+            out += tot;
+            __syncthreads();                    // wsum reuse; this chunk's writes precede the next chunk's reads
+        }
+        if (threadIdx.x == 0) live_len[x] = out;
+    }
+}
+
+__global__ void k_alive_list(const uint8_t* __restrict__ alive, int64_t m, int32_t* __restrict__ list,
+                             int* __restrict__ count) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const bool in = alive[e] != 0;
+        const unsigned ballot = __ballot_sync(__activemask(), in);
+        if (in) {
+            const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(count, __popc(ballot));
+            base = __shfl_sync(ballot, base, leader);
+            list[base + __popc(ballot & ((1u << lane) - 1))] = (int32_t)e;
+        }
+    }
+}
+
+// X = {alive e : S(e) < thr}, over the live-edge list (list == nullptr: all e < m)
+__global__ void k_frontier_scan(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive,
+                                const int32_t* __restrict__ list, int64_t len, uint32_t thr,
+                                int32_t* __restrict__ rem, int32_t round, int32_t* __restrict__ front,
+                                int* __restrict__ count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = list ? (int64_t)list[i] : i;
         bool in = alive[e] && S[e] < thr;
         unsigned ballot = __ballot_sync(__activemask(), in);
         if (in) {
@@ -93,7 +207,8 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a
 // One warp per frontier edge e = (a, b): destroy its live triangles.
 __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front, int nfront,
                                               const int32_t* __restrict__ dag_src, const int32_t* __restrict__ dag_col,
-                                              const int64_t* __restrict__ sym_ptr, const int32_t* __restrict__ sym_col,
+                                              const int64_t* __restrict__ sym_ptr, const int32_t* __restrict__ live_len,
+                                              const int32_t* __restrict__ sym_col,
                                               const int32_t* __restrict__ sym_eid, const uint8_t* __restrict__ alive,
                                               int32_t* __restrict__ rem, uint32_t* __restrict__ S, uint32_t thr,
                                               int32_t round, int32_t* __restrict__ next, int* __restrict__ next_count) {
@@ -108,7 +223,7 @@ __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front,
         const uint32_t live = S[e];
         if (live == 0) continue;
         const int a = dag_src[e], b = dag_col[e];
-        int64_t a0 = sym_ptr[a], a1 = sym_ptr[a + 1], b0 = sym_ptr[b], b1 = sym_ptr[b + 1];
+        int64_t a0 = sym_ptr[a], a1 = a0 + live_len[a], b0 = sym_ptr[b], b1 = b0 + live_len[b];
         // iterate the shorter row, search the longer
         if (a1 - a0 > b1 - b0) {
             int64_t t0 = a0, t1 = a1;
@@ -204,6 +319,7 @@ __global__ void __launch_bounds__(256) k_peel_part(const int32_t* __restrict__ f
                                                    const int32_t* __restrict__ dag_src,
                                                    const int32_t* __restrict__ dag_col,
                                                    const int64_t* __restrict__ sym_ptr,
+                                                   const int32_t* __restrict__ live_len,
                                                    const int32_t* __restrict__ sym_col,
                                                    const int32_t* __restrict__ sym_eid,
                                                    const uint8_t* __restrict__ alive, const uint32_t* __restrict__ xbits,
@@ -220,7 +336,7 @@ __global__ void __launch_bounds__(256) k_peel_part(const int32_t* __restrict__ f
         const uint32_t live = own_e ? S[e] : 0xFFFFFFFFu;
         if (live == 0) continue;
         const int a = dag_src[e], b = dag_col[e];
-        int64_t a0 = sym_ptr[a], a1 = sym_ptr[a + 1], b0 = sym_ptr[b], b1 = sym_ptr[b + 1];
+        int64_t a0 = sym_ptr[a], a1 = a0 + live_len[a], b0 = sym_ptr[b], b1 = b0 + live_len[b];
         if (a1 - a0 > b1 - b0) {
             int64_t t0 = a0, t1 = a1;
             a0 = b0; a1 = b1; b0 = t0; b1 = t1;
@@ -284,14 +400,56 @@ int build_sym(gc_ctx* c) {
     GC_TRY(ensure(c, c->sym_ptr, (size_t)(n + 1) * 8));
     GC_TRY(ensure(c, c->sym_col, (size_t)2 * m * 4));
     GC_TRY(ensure(c, c->sym_eid, (size_t)2 * m * 4));
+    GC_TRY(ensure(c, c->live_len, (size_t)n * 4));
+    GC_TRY(ensure(c, c->long_rows, (size_t)n * 4));
     GC_LAUNCH(c, k_sym_ptr, grid_for(n + 1), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(), n,
               c->sym_ptr.as<int64_t>());
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 232);
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
+    if (n > 0)
+        GC_LAUNCH(c, k_long_rows, grid_for(n), kThreads, 0, c->sym_ptr.as<int64_t>(), n, c->long_rows.as<int32_t>(),
+                  cnt);
+    GC_CUDA(c, cudaMemcpyAsync(c->hpin, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    c->nlong = *static_cast<int*>(c->hpin);
+    c->sym_ready = true;
+    c->sym_dirty = true;
+    return GC_OK;
+}
+
+// (Re)fill the symmetric rows from the DAG: every entry live, full lengths.
+static int sym_refill(gc_ctx* c) {
+    const int64_t n = c->n, m = c->m;
     if (m > 0)
         GC_LAUNCH(c, k_sym_fill, grid_for(m), kThreads, 0, c->in_src.as<int32_t>(), c->in_dst.as<int32_t>(),
                   c->in_pos.as<int32_t>(), c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
                   c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(), m, c->sym_col.as<int32_t>(),
                   c->sym_eid.as<int32_t>());
-    c->sym_ready = true;
+    if (n > 0)
+        GC_LAUNCH(c, k_live_len_init, grid_for(n), kThreads, 0, c->sym_ptr.as<int64_t>(), n,
+                  c->live_len.as<int32_t>());
+    c->sym_dirty = false;
+    return GC_OK;
+}
+
+// Drop dead entries from the rows once the live edge count has fallen to
+// 1/compact_div of what it was at the last compaction (or the start).
+static int maybe_compact(gc_ctx* c) {
+    if (c->compact_div <= 1 || c->m_alive_h <= 0 || c->m_alive_h * c->compact_div > c->compact_at) return GC_OK;
+    const int64_t n = c->n, m = c->m;
+    GC_LAUNCH(c, k_row_compact_warp, grid_for(n * 32), kThreads, 0, c->sym_ptr.as<int64_t>(),
+              c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), n);
+    if (c->nlong > 0)
+        GC_LAUNCH(c, k_row_compact_block, std::min(c->nlong, 148 * 8), 256, 0, c->long_rows.as<int32_t>(), c->nlong,
+                  c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                  c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>());
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 232);
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
+    GC_LAUNCH(c, k_alive_list, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, c->alist.as<int32_t>(), cnt);
+    c->alist_n = c->m_alive_h;
+    c->compact_at = c->m_alive_h;
+    c->sym_dirty = true;              // the next peel call refills the rows
+    c->stats.compactions++;
     return GC_OK;
 }
 
@@ -302,9 +460,12 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
     int32_t* h = static_cast<int32_t*>(c->hpin);
     *removed = 0;
+    GC_TRY(maybe_compact(c));
     GC_CUDA(c, cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
-    GC_LAUNCH(c, k_frontier_scan, grid_for(m), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), m, thr,
-              c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt);
+    const int32_t* list = c->alist_n >= 0 ? c->alist.as<int32_t>() : nullptr;
+    const int64_t len = c->alist_n >= 0 ? c->alist_n : m;
+    GC_LAUNCH(c, k_frontier_scan, grid_for(len), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), list,
+              len, thr, c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt);
     GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
     int nf = h[0];
@@ -315,16 +476,19 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         GC_CUDA(c, cudaMemsetAsync(ncnt, 0, sizeof(int), c->stream));
         const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
         GC_LAUNCH(c, k_peel, blocks, 256, 0, cur, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
-                  c->sym_ptr.as<int64_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
-                  c->alive.as<uint8_t>(), c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, nxt, ncnt);
+                  c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                  c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr,
+                  *round, nxt, ncnt);
         GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, cur, nf, c->alive.as<uint8_t>(),
                   level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
         GC_CUDA(c, cudaMemcpyAsync(h, ncnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         GC_TRY(sync(c));
         *removed += nf;
+        c->m_alive_h -= nf;
         ++*round;
         c->stats.peel_rounds++;
         nf = h[0];
+        GC_TRY(maybe_compact(c));
         int32_t* t = cur;
         cur = nxt;
         nxt = t;
@@ -362,6 +526,7 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
     auto lo_of = [&](int r) { return std::min<int64_t>(m, (int64_t)r * W * 32); };
     auto hi_of = [&](int r) { return std::min<int64_t>(m, (int64_t)(r + 1) * W * 32); };
     // X at the level start: each owner scans its range
+    GC_TRY(maybe_compact(c));
     GC_CUDA(c, cudaMemsetAsync(xb, 0, (size_t)P * W * 4, c->stream));
     for (int r = r_begin; r < r_end; ++r)
         if (hi_of(r) > lo_of(r))
@@ -379,13 +544,16 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
         for (int r = r_begin; r < r_end; ++r)
             GC_LAUNCH(c, k_peel_part, blocks, 256, 0, front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
-                      c->sym_ptr.as<int64_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
-                      c->alive.as<uint8_t>(), xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb);
+                      c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                      c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), xb, part_support(c, r), thr, lo_of(r),
+                      hi_of(r), nb);
         GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, front, nf, c->alive.as<uint8_t>(),
                   level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
         *removed += nf;
+        c->m_alive_h -= nf;
         c->stats.peel_rounds++;
         std::swap(xb, nb);
+        GC_TRY(maybe_compact(c));
     }
     return GC_OK;
 }
@@ -397,13 +565,19 @@ static int peel_setup(gc_ctx* c) {
     GC_TRY(ensure(c, c->rem, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_a, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_b, (size_t)m * 4));
+    GC_TRY(ensure(c, c->alist, (size_t)m * 4));
     GC_TRY(ensure(c, c->scal, 1024));
     GC_TRY(host_scratch(c, 4096));
+    if (c->sym_dirty) GC_TRY(sym_refill(c));
+    c->m_alive_h = m;
+    c->compact_at = m;
+    c->alist_n = -1;
     if (m > 0) {
         GC_LAUNCH(c, k_fill_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, (uint8_t)1);
         GC_LAUNCH(c, k_fill_i32, grid_for(m), kThreads, 0, c->rem.as<int32_t>(), m, (int32_t)-1);
     }
     c->stats.peel_rounds = 0;
+    c->stats.compactions = 0;
     const int P = peel_parts(c);
     if (P > 0) {
         const int64_t W = part_words(c, P);

@@ -39,6 +39,7 @@ GC_OPT_BLOCK_BATCH = 6
 GC_OPT_SUP_UW = 7
 GC_OPT_PEEL_PART = 8
 GC_OPT_HUGE_MAX = 9
+GC_OPT_COMPACT = 10
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -55,6 +56,7 @@ class gc_stats(ctypes.Structure):
         ("support_ms", ctypes.c_double), ("support_kernel_ms", ctypes.c_double),
         ("ktruss_ms", ctypes.c_double), ("peel_ms", ctypes.c_double), ("decomp_ms", ctypes.c_double),
         ("launches", ctypes.c_int64), ("lib_launches", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
+        ("compactions", ctypes.c_int64),
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("wedges", ctypes.c_int64),
         ("q_out", ctypes.c_int64), ("q_in", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
         ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),

@@ -11,6 +11,7 @@ p.add_argument("--ks", default="")
 p.add_argument("--part", type=int, default=0)
 p.add_argument("--loop", type=int, default=0)
 p.add_argument("--tc", type=int, default=0)
+p.add_argument("--compact", type=int, default=-1)
 p.add_argument("--no-decomp", action="store_true")
 a = p.parse_args()
 t0 = time.time()
@@ -19,6 +20,8 @@ print(f"gen {time.time()-t0:.1f}s nnz={u.size}", flush=True)
 ctx = gc.Context(0, torch.cuda.current_stream())
 if a.loop:
     ctx.comm_init_loopback(a.loop)
+if a.compact >= 0:
+    ctx.set_option(gc.GC_OPT_COMPACT, a.compact)
 if a.part:
     ctx.set_option(gc.GC_OPT_PEEL_PART, 1)
 ctx.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
@@ -46,4 +49,4 @@ tau = torch.empty(m, dtype=torch.int32, device="cuda")
 t0 = time.time()
 _, kmax = ctx.truss_decomposition(tau)
 st = ctx.stats()
-print(f"decomposition: kmax={kmax} {st['decomp_ms']:.1f} ms (peel {st['peel_ms']:.1f} ms, {st['peel_rounds']} rounds) wall {time.time()-t0:.2f}s", flush=True)
+print(f"decomposition: kmax={kmax} {st['decomp_ms']:.1f} ms (peel {st['peel_ms']:.1f} ms, {st['peel_rounds']} rounds, {st['compactions']} compactions) wall {time.time()-t0:.2f}s", flush=True)

@@ -348,6 +348,29 @@ def test_loopback_partitions(gcmod, parts):
         assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
+@pytest.mark.parametrize("compact", [0, 2, 3])
+def test_decomposition_row_compaction(gcmod, compact):
+    """Peeler with dead-entry compaction of the adjacency rows off / every
+    halving / every third (C1 decomposition and k-truss, R-MAT s12)."""
+    for u, v in [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=29)]:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            c.set_option(gcmod.GC_OPT_COMPACT, compact)
+            c.load_edges(u, v)
+            c.build_csr()
+            for k in (5, 9):
+                want, _ = g.ktruss(k)
+                assert np.array_equal(c.ktruss(k)[0], want), k
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax = g.truss_decomposition()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax
+            if compact:
+                assert c.stats()["compactions"] > 0
+            # a second call after compaction starts from refilled rows
+            want, _ = g.ktruss(4)
+            assert np.array_equal(c.ktruss(4)[0], want)
+
+
 @pytest.mark.parametrize("parts", [1, 2, 5])
 def test_partitioned_peeler_c1_and_fixtures(gcmod, parts):
     """The multi-GPU peeler (removed-edge bitmap per round, owner-only
