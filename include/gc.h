@@ -197,6 +197,9 @@ typedef struct gc_stats {
     double ktruss_ms;         /* last gc_ktruss (support + peel) */
     double peel_ms;           /* peel part of the last gc_ktruss / decomposition */
     double decomp_ms;         /* last gc_truss_decomposition */
+    double peel_kernel_ms;    /* triangle-destroying kernels of the last peel (sum) */
+    double scan_ms;           /* level frontier scans of the last peel (sum) */
+    double compact_ms;        /* dead-entry compactions of the last peel (sum) */
     int64_t launches;         /* libgc kernel launches since gc_reset_stats */
     int64_t lib_launches;     /* CUB (library) kernel launches, estimated, same window */
     int64_t peel_rounds;      /* rounds of the last peel (ktruss or decomposition) */

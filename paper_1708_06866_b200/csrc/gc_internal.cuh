@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "gc.h"
@@ -118,6 +119,7 @@ struct gc_ctx {
     int64_t alist_n = -1;       // -1: no list (scan every edge)
     int64_t m_alive_h = 0;      // live edges (host mirror)
     int64_t compact_at = 0;     // live edges at the last compaction
+    int trace = getenv("GC_PEEL_TRACE") != nullptr;   // diagnostics: one stderr line per peel round
     int compact_div = 2;        // compact when live edges fall to 1/compact_div (GC_OPT_COMPACT; <= 1 never)
     gcx::Buf alive;     // uint8[m]
     gcx::Buf rem;       // int32[m] round in which the edge is in the frontier
@@ -133,7 +135,7 @@ struct gc_ctx {
     size_t hpin_cap = 0;
 
     // events
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[14] = {};   // 0-7 phases; 8-13 peel sub-phases (kernel / scan / compaction)
 
     gc_stats stats = {};
 

@@ -204,27 +204,79 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a
     return lo;
 }
 
-// One warp per frontier edge e = (a, b): destroy its live triangles.
-__global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front, int nfront,
-                                              const int32_t* __restrict__ dag_src, const int32_t* __restrict__ dag_col,
-                                              const int64_t* __restrict__ sym_ptr, const int32_t* __restrict__ live_len,
-                                              const int32_t* __restrict__ sym_col,
-                                              const int32_t* __restrict__ sym_eid, const uint8_t* __restrict__ alive,
-                                              int32_t* __restrict__ rem, uint32_t* __restrict__ S, uint32_t thr,
-                                              int32_t round, int32_t* __restrict__ next, int* __restrict__ next_count) {
+// Round semantics (reading A5): a triangle alive at the round start with at
+// least one edge in X is handled only by its smallest-id edge in X, which
+// decrements each surviving edge once.  The two policies differ in how X is
+// represented and which survivors a rank may decrement.
+struct PolicySingle {       // one rank: X = {rem == round}; crossings append to the next list
+    int32_t* rem;
+    uint32_t* S;
+    uint32_t thr;
+    int32_t round;
+    int32_t* next;
+    int* next_count;
+    __device__ __forceinline__ uint32_t live(int e) const { return S[e]; }   // exact at round start
+    __device__ __forceinline__ bool in_x(int f) const { return rem[f] == round; }
+    __device__ __forceinline__ void dec(int f) const {
+        if (atomicSub(S + f, 1u) == thr) {
+            rem[f] = round + 1;
+            next[atomicAdd(next_count, 1)] = f;
+        }
+    }
+};
+
+struct PolicyPart {         // P ranks: X as a bitmap; only owned edges [lo, hi) are decremented
+    const uint32_t* xbits;
+    uint32_t* S;
+    uint32_t thr;
+    int64_t lo, hi;
+    uint32_t* nbits;
+    // S(e) is exact only for owned e (an upper bound otherwise)
+    __device__ __forceinline__ uint32_t live(int e) const { return (e >= lo && e < hi) ? S[e] : 0xFFFFFFFFu; }
+    __device__ __forceinline__ bool in_x(int f) const { return (xbits[f >> 5] >> (f & 31)) & 1u; }
+    __device__ __forceinline__ void dec(int f) const {
+        if (f >= lo && f < hi && atomicSub(S + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
+    }
+};
+
+template <class Pol>
+__device__ __forceinline__ void destroy(const Pol& pol, int e, int f, int g) {
+    const bool fx = pol.in_x(f), gx = pol.in_x(g);
+    if ((fx && f < e) || (gx && g < e)) return;   // a smaller X-edge owns this triangle
+    if (!fx) pol.dec(f);
+    if (!gx) pol.dec(g);
+}
+
+struct PeelArgs {
+    const int32_t* front;
+    int nfront;
+    const int32_t* dag_src;
+    const int32_t* dag_col;
+    const int64_t* sym_ptr;
+    const int32_t* live_len;
+    const int32_t* sym_col;
+    const int32_t* sym_eid;
+    const uint8_t* alive;
+};
+
+// One warp per frontier edge e = (a, b): destroy its live triangles by
+// walking the shorter endpoint row (lanes over its entries) and binary-
+// searching each live entry in the longer one (rows sorted by rank; dead
+// entries compacted away now and then).  Stop once S(e) live triangles are
+// found (S exact only for the single-rank policy).  Measured alternatives
+// (DESIGN.md): one lane per short-row edge, 32-ary window narrowing, and
+// splitting long rows into work items over many warps were all slower at C4
+// and C5, where the big early rounds dominate.
+template <class Pol>
+__global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
-        const int e = front[wi];
-        // S(e) is exact at round start (every destroyed triangle decremented its
-        // survivors) and frontier edges are not decremented in their own round:
-        // it is the number of live triangles through e.  None: nothing to do
-        // (the whole k = 3 peel); otherwise stop once all S(e) are found.
-        const uint32_t live = S[e];
-        if (live == 0) continue;
-        const int a = dag_src[e], b = dag_col[e];
-        int64_t a0 = sym_ptr[a], a1 = a0 + live_len[a], b0 = sym_ptr[b], b1 = b0 + live_len[b];
-        // iterate the shorter row, search the longer
+    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < A.nfront; wi += warps) {
+        const int e = A.front[wi];
+        const uint32_t live = pol.live(e);
+        if (live == 0) continue;                 // no live triangle (the whole k = 3 peel)
+        const int a = A.dag_src[e], b = A.dag_col[e];
+        int64_t a0 = A.sym_ptr[a], a1 = a0 + A.live_len[a], b0 = A.sym_ptr[b], b1 = b0 + A.live_len[b];
         if (a1 - a0 > b1 - b0) {
             int64_t t0 = a0, t1 = a1;
             a0 = b0; a1 = b1; b0 = t0; b1 = t1;
@@ -235,34 +287,18 @@ __global__ void __launch_bounds__(256) k_peel(const int32_t* __restrict__ front,
             bool tri = false;
             int f = -1, g = -1;
             if (i < a1) {
-                f = __ldg(sym_eid + i);
-                if (f != e && alive[f]) {
-                    const int32_t w = __ldg(sym_col + i);
-                    const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
-                    if (j < b1 && __ldg(sym_col + j) == w) {
-                        g = __ldg(sym_eid + j);
-                        tri = alive[g] != 0;
+                f = __ldg(A.sym_eid + i);
+                if (f != e && A.alive[f]) {
+                    const int32_t w = __ldg(A.sym_col + i);
+                    const int64_t j = lower_bound_i32(A.sym_col, b0, b1, w);
+                    if (j < b1 && __ldg(A.sym_col + j) == w) {
+                        g = __ldg(A.sym_eid + j);
+                        tri = A.alive[g] != 0;
                     }
                 }
             }
             found += __popc(__ballot_sync(0xffffffffu, tri));
-            if (!tri) continue;
-            const bool fx = rem[f] == round, gx = rem[g] == round;
-            if ((fx && f < e) || (gx && g < e)) continue;   // a smaller X-edge owns this triangle
-            if (!fx) {
-                uint32_t old = atomicSub(S + f, 1u);
-                if (old == thr) {
-                    rem[f] = round + 1;
-                    next[atomicAdd(next_count, 1)] = f;
-                }
-            }
-            if (!gx) {
-                uint32_t old = atomicSub(S + g, 1u);
-                if (old == thr) {
-                    rem[g] = round + 1;
-                    next[atomicAdd(next_count, 1)] = g;
-                }
-            }
+            if (tri) destroy(pol, e, f, g);
         }
     }
 }
@@ -309,64 +345,6 @@ __global__ void k_bits_to_list(const uint32_t* __restrict__ bits, int64_t nwords
             const int b = __ffs(x) - 1;
             x &= x - 1;
             list[base++] = (int32_t)(w * 32 + b);
-        }
-    }
-}
-
-// k_peel with X given as a bitmap and decrements restricted to owned edges
-// [lo, hi); an owned survivor crossing thr -> thr-1 sets its bit in nbits.
-__global__ void __launch_bounds__(256) k_peel_part(const int32_t* __restrict__ front, int nfront,
-                                                   const int32_t* __restrict__ dag_src,
-                                                   const int32_t* __restrict__ dag_col,
-                                                   const int64_t* __restrict__ sym_ptr,
-                                                   const int32_t* __restrict__ live_len,
-                                                   const int32_t* __restrict__ sym_col,
-                                                   const int32_t* __restrict__ sym_eid,
-                                                   const uint8_t* __restrict__ alive, const uint32_t* __restrict__ xbits,
-                                                   uint32_t* __restrict__ S, uint32_t thr, int64_t lo, int64_t hi,
-                                                   uint32_t* __restrict__ nbits) {
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    auto in_x = [&](int f) { return (xbits[f >> 5] >> (f & 31)) & 1u; };
-    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
-        const int e = front[wi];
-        // S(e) is exact only when e is owned (an upper bound otherwise): it
-        // may end the search early only then.
-        const bool own_e = e >= lo && e < hi;
-        const uint32_t live = own_e ? S[e] : 0xFFFFFFFFu;
-        if (live == 0) continue;
-        const int a = dag_src[e], b = dag_col[e];
-        int64_t a0 = sym_ptr[a], a1 = a0 + live_len[a], b0 = sym_ptr[b], b1 = b0 + live_len[b];
-        if (a1 - a0 > b1 - b0) {
-            int64_t t0 = a0, t1 = a1;
-            a0 = b0; a1 = b1; b0 = t0; b1 = t1;
-        }
-        uint32_t found = 0;
-        for (int64_t base = a0; base < a1 && found < live; base += 32) {
-            const int64_t i = base + lane;
-            bool tri = false;
-            int f = -1, g = -1;
-            if (i < a1) {
-                f = __ldg(sym_eid + i);
-                if (f != e && alive[f]) {
-                    const int32_t w = __ldg(sym_col + i);
-                    const int64_t j = lower_bound_i32(sym_col, b0, b1, w);
-                    if (j < b1 && __ldg(sym_col + j) == w) {
-                        g = __ldg(sym_eid + j);
-                        tri = alive[g] != 0;
-                    }
-                }
-            }
-            found += __popc(__ballot_sync(0xffffffffu, tri));
-            if (!tri) continue;
-            const bool fx = in_x(f), gx = in_x(g);
-            if ((fx && f < e) || (gx && g < e)) continue;   // a smaller X-edge owns this triangle
-            if (!fx && f >= lo && f < hi) {
-                if (atomicSub(S + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
-            }
-            if (!gx && g >= lo && g < hi) {
-                if (atomicSub(S + g, 1u) == thr) atomicOr(nbits + (g >> 5), 1u << (g & 31));
-            }
         }
     }
 }
@@ -437,6 +415,7 @@ static int sym_refill(gc_ctx* c) {
 static int maybe_compact(gc_ctx* c) {
     if (c->compact_div <= 1 || c->m_alive_h <= 0 || c->m_alive_h * c->compact_div > c->compact_at) return GC_OK;
     const int64_t n = c->n, m = c->m;
+    GC_TRY(record(c, 12));
     GC_LAUNCH(c, k_row_compact_warp, grid_for(n * 32), kThreads, 0, c->sym_ptr.as<int64_t>(),
               c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), n);
     if (c->nlong > 0)
@@ -446,10 +425,24 @@ static int maybe_compact(gc_ctx* c) {
     int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 232);
     GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
     GC_LAUNCH(c, k_alive_list, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, c->alist.as<int32_t>(), cnt);
+    GC_TRY(record(c, 13));
+    GC_TRY(sync(c));
+    c->stats.compact_ms += elapsed(c, 12, 13);
     c->alist_n = c->m_alive_h;
     c->compact_at = c->m_alive_h;
     c->sym_dirty = true;              // the next peel call refills the rows
     c->stats.compactions++;
+    return GC_OK;
+}
+
+// One peel round over the frontier list.
+template <class Pol>
+static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
+    PeelArgs A{front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(), c->sym_ptr.as<int64_t>(),
+               c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
+               c->alive.as<uint8_t>()};
+    const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
+    GC_LAUNCH(c, k_peel<Pol>, blocks, 256, 0, A, pol);
     return GC_OK;
 }
 
@@ -464,25 +457,29 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     GC_CUDA(c, cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
     const int32_t* list = c->alist_n >= 0 ? c->alist.as<int32_t>() : nullptr;
     const int64_t len = c->alist_n >= 0 ? c->alist_n : m;
+    GC_TRY(record(c, 10));
     GC_LAUNCH(c, k_frontier_scan, grid_for(len), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), list,
               len, thr, c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt);
+    GC_TRY(record(c, 11));
     GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
+    c->stats.scan_ms += elapsed(c, 10, 11);
     int nf = h[0];
     int32_t* cur = c->front_a.as<int32_t>();
     int32_t* nxt = c->front_b.as<int32_t>();
     int* ncnt = cnt + 1;
     while (nf > 0) {
         GC_CUDA(c, cudaMemsetAsync(ncnt, 0, sizeof(int), c->stream));
-        const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
-        GC_LAUNCH(c, k_peel, blocks, 256, 0, cur, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
-                  c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
-                  c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr,
-                  *round, nxt, ncnt);
+        GC_TRY(record(c, 8));
+        PolicySingle pol{c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, nxt, ncnt};
+        GC_TRY(peel_round(c, cur, nf, pol));
+        GC_TRY(record(c, 9));
         GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, cur, nf, c->alive.as<uint8_t>(),
                   level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
         GC_CUDA(c, cudaMemcpyAsync(h, ncnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         GC_TRY(sync(c));
+        c->stats.peel_kernel_ms += elapsed(c, 8, 9);
+        if (c->trace) fprintf(stderr, "peel-trace level %d round %d nf %d ms %.4f\n", level, *round, nf, elapsed(c, 8, 9));
         *removed += nf;
         c->m_alive_h -= nf;
         ++*round;
@@ -541,12 +538,10 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         const int nf = h[0];
         if (nf == 0) break;
         GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
-        const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
-        for (int r = r_begin; r < r_end; ++r)
-            GC_LAUNCH(c, k_peel_part, blocks, 256, 0, front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
-                      c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
-                      c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>(), xb, part_support(c, r), thr, lo_of(r),
-                      hi_of(r), nb);
+        for (int r = r_begin; r < r_end; ++r) {
+            PolicyPart pol{xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb};
+            GC_TRY(peel_round(c, front, nf, pol));
+        }
         GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, front, nf, c->alive.as<uint8_t>(),
                   level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
         *removed += nf;
@@ -578,6 +573,7 @@ static int peel_setup(gc_ctx* c) {
     }
     c->stats.peel_rounds = 0;
     c->stats.compactions = 0;
+    c->stats.peel_kernel_ms = c->stats.scan_ms = c->stats.compact_ms = 0;
     const int P = peel_parts(c);
     if (P > 0) {
         const int64_t W = part_words(c, P);

@@ -55,6 +55,7 @@ class gc_stats(ctypes.Structure):
         ("build_ms", ctypes.c_double), ("tc_ms", ctypes.c_double), ("tc_kernel_ms", ctypes.c_double),
         ("support_ms", ctypes.c_double), ("support_kernel_ms", ctypes.c_double),
         ("ktruss_ms", ctypes.c_double), ("peel_ms", ctypes.c_double), ("decomp_ms", ctypes.c_double),
+        ("peel_kernel_ms", ctypes.c_double), ("scan_ms", ctypes.c_double), ("compact_ms", ctypes.c_double),
         ("launches", ctypes.c_int64), ("lib_launches", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
         ("compactions", ctypes.c_int64),
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("wedges", ctypes.c_int64),

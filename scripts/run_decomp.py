@@ -49,4 +49,5 @@ tau = torch.empty(m, dtype=torch.int32, device="cuda")
 t0 = time.time()
 _, kmax = ctx.truss_decomposition(tau)
 st = ctx.stats()
-print(f"decomposition: kmax={kmax} {st['decomp_ms']:.1f} ms (peel {st['peel_ms']:.1f} ms, {st['peel_rounds']} rounds, {st['compactions']} compactions) wall {time.time()-t0:.2f}s", flush=True)
+print(f"decomposition: kmax={kmax} {st['decomp_ms']:.1f} ms (peel {st['peel_ms']:.1f} ms, {st['peel_rounds']} rounds, {st['compactions']} compactions) wall {time.time()-t0:.2f}s "
+      f"kernel {st['peel_kernel_ms']:.1f} scan {st['scan_ms']:.1f} compact {st['compact_ms']:.1f} ms", flush=True)

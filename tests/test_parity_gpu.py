@@ -246,6 +246,45 @@ def test_c4_full_size_sampled(gcmod):
     assert np.all(h.support_pairs(g.cu[keep][sample], g.cv[keep][sample]) >= 1)
 
 
+def test_c5_full_size_sampled(gcmod):
+    """BASELINE configs[4] (skewed R-MAT s26, ~9.3e8 edges) on one GPU: sampled
+    supports against the oracle, T = Σ support / 3, and the full truss
+    decomposition checked for soundness at its top levels: every sampled edge
+    of H_t = {e : τ(e) >= t} has at least t-2 triangles inside H_t (so H_t lies
+    in the t-truss), H_kmax is non-empty, τ >= 2 everywhere.  (The oracle's own
+    decomposition of C5 takes hours; parity on C1-C3 covers exactness.)"""
+    import torch
+    u, v = gen.CONFIGS["C5"].generate()
+    c = gcmod.Context(0, torch.cuda.current_stream())
+    try:
+        c.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+        c.build_csr()
+        m = c.num_edges()
+        T = c.triangle_count()
+        sup = c.edge_support()
+        tau, kmax = c.truss_decomposition()
+    finally:
+        c.close()
+    assert int(sup.astype(np.int64).sum()) == 3 * T
+    g = oracle.OracleGraph(u, v)
+    del u, v
+    assert g.m == m
+    rng = np.random.default_rng(5)
+    idx = np.sort(rng.choice(m, size=20000, replace=False))
+    assert np.array_equal(sup[idx], g.support_pairs(g.cu[idx], g.cv[idx]))
+    assert tau.min() >= 2 and tau.max() == kmax and kmax >= 3
+    # soundness of the top levels (H_t small enough for the oracle)
+    levels = sorted({kmax, kmax - 1, int(np.quantile(tau[tau > 2], 0.999))}, reverse=True)
+    for t in levels:
+        keep = np.flatnonzero(tau >= t)
+        assert keep.size > 0
+        if keep.size > 60_000_000:
+            continue
+        h = oracle.OracleGraph(g.cu[keep], g.cv[keep])
+        sample = rng.choice(keep.size, size=min(20000, keep.size), replace=False)
+        assert np.all(h.support_pairs(g.cu[keep][sample], g.cv[keep][sample]) >= t - 2), t
+
+
 # ------------------------------------------------------- kernel class forcing --
 @pytest.mark.parametrize("force", [0, 1, 2, 3])
 def test_forced_classes(ctx, gcmod, force):
