@@ -136,7 +136,8 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
 // [ca, cb) are visited: in-edge i owns cost units [in_cost[i], in_cost[i] +
 // kOvh + len) and its wedge j sits at unit in_cost[i] + kOvh + j, so disjoint
 // unit ranges split a task's wedges exactly (the block kernel gives each
-// warp one eighth).  probe.find(w) returns the slot/index of w in N+(v) or -1.
+// warp one eighth).  probe.loc(w) returns a handle (>= 0) when w is in N+(v), else -1;
+// probe.credit(handle) adds the (v,w)-role credit.
 template <bool SUP, bool CLIP, class Probe>
 __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int64_t cb,
                                                 const int32_t* __restrict__ in_pos,
@@ -175,11 +176,15 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             uint32_t seg_hits = 0;
             auto visit = [&](int q, int w) {
                 const uint32_t inr = (uint32_t)(q - b) < (uint32_t)(e - b);
-                const uint32_t h = inr & probe.hit((uint32_t)w);  // branch-free for the bitmap
-                seg_hits += h;
-                if (SUP && h) {
-                    probe.credit(probe.find((uint32_t)w), sup);   // role (v,w)
-                    if (uw == 0) atomicAdd(sup + q, 1u);          // role (u,w)
+                if (!SUP) {
+                    seg_hits += inr & probe.hit((uint32_t)w);     // branch-free for the bitmap
+                } else {
+                    const int hd = probe.loc((uint32_t)w);        // located once
+                    if (inr && hd >= 0) {
+                        ++seg_hits;
+                        probe.credit(hd, sup);                    // role (v,w)
+                        if (uw == 0) atomicAdd(sup + q, 1u);      // role (u,w)
+                    }
                 }
             };
             // a vector wholly inside [b, e) needs no per-element bounds checks
@@ -234,7 +239,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                 if (!SUP) {
                     hits += probe.hit(w);
                 } else {
-                    const int slot = probe.find(w);
+                    const int slot = probe.loc(w);
                     if (slot >= 0) {
                         hit = true;
                         ++hits;
@@ -275,6 +280,7 @@ struct SmemHash {
             h = (h + 1) & mask;
         }
     }
+    __device__ __forceinline__ int loc(uint32_t w) const { return find(w); }
     __device__ __forceinline__ void credit(int slot, uint32_t*) const {
         if (SUP) atomicAdd(cnt + slot, 1u);
     }
@@ -385,19 +391,21 @@ struct SmemBitmap {
         const uint32_t word = g_dsmem[min(x >> 5, (uint32_t)(kBW - 1))];
         return (word >> (x & 31)) & 1u;
     }
-    __device__ __forceinline__ int find(uint32_t w) const {
+    // handle of a member = its window offset x (branch-free test as in hit())
+    __device__ __forceinline__ int loc(uint32_t w) const {
         const uint32_t x = w - base;
-        if (x >= nbits) return -1;
-        const uint32_t word = bits[x >> 5];
-        const uint32_t bit = 1u << (x & 31);
-        if (!(word & bit)) return -1;
-        if (!SUP) return 0;
-        // pre holds the index of the first element of each 64-bit chunk
-        const uint32_t lo = (x & 32) ? bits[(x >> 5) - 1] : 0u;   // lower word of the chunk
-        return (int)pre[x >> 6] + __popc(lo) + __popc(word & (bit - 1));
+        const uint32_t word = g_dsmem[min(x >> 5, (uint32_t)(kBW - 1))];
+        return ((word >> (x & 31)) & 1u) ? (int)x : -1;
     }
-    __device__ __forceinline__ void credit(int j, uint32_t*) const {
-        if (SUP) atomicAdd(cnt + j, 1u);
+    // role (v,w): the index j of w in N+(v) = set bits before x; pre holds the
+    // index of the first element of each 64-bit chunk
+    __device__ __forceinline__ void credit(int hd, uint32_t*) const {
+        if (!SUP) return;
+        const uint32_t x = (uint32_t)hd;
+        const uint32_t word = bits[x >> 5];
+        const uint32_t lo = (x & 32) ? bits[(x >> 5) - 1] : 0u;   // lower word of the chunk
+        const int j = (int)pre[x >> 6] + __popc(lo) + __popc(word & ((1u << (x & 31)) - 1u));
+        atomicAdd(cnt + j, 1u);
     }
 };
 
@@ -432,6 +440,7 @@ struct GlobalProbe {
         }
         return (lo < d && (uint32_t)__ldg(row + lo) == w) ? lo : -1;
     }
+    __device__ __forceinline__ int loc(uint32_t w) const { return find(w); }
     __device__ __forceinline__ void credit(int j, uint32_t* sup) const { atomicAdd(sup + r0 + j, 1u); }
     __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
