@@ -170,9 +170,9 @@ typedef enum gc_option {
                                  batches dealt round-robin (default 32; tuning) */
     GC_OPT_BLOCK_BITMAP = 4,  /* 1: heavy-head kernel may use the rank-window bitmap
                                  (default); 0: always its hash table (testing) */
-    GC_OPT_SUP_UW = 7,        /* (u,w)-role support credits: 0 one global atomic per
-                                 triangle; 1 wedge hit-bitmap + per-row column sums;
-                                 99 skipped (timing diagnostics only: wrong supports) */
+    GC_OPT_SUP_SKIP = 7,      /* timing diagnostics only (wrong supports when nonzero):
+                                 mask of support roles to skip, 1 (u,w), 2 (v,w),
+                                 4 (u,v); default 0 */
     GC_OPT_PEEL_PART = 8,     /* 1: use the partitioned k-truss peeler (removed-edge
                                  bitmap per round, owner-only decrements; the multi-GPU
                                  path) even on a single rank (testing); it is always

@@ -373,9 +373,9 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
                 GC_TRY(sync(c));
             }
             return GC_OK;
-        case GC_OPT_SUP_UW:
-            if (value != 0 && value != 1 && value != 99) return fail(c, GC_ERR_INVALID, "sup_uw must be 0, 1 or 99");
-            c->sup_uw = (int)value;
+        case GC_OPT_SUP_SKIP:
+            if (value < 0 || value > 7) return fail(c, GC_ERR_INVALID, "support skip mask must be 0..7");
+            c->sup_skip = (int)value;
             return GC_OK;
         case GC_OPT_HUGE_MAX:
             if (value < 0 || value > 8192) return fail(c, GC_ERR_INVALID, "huge-head hash limit must be 0..8192");

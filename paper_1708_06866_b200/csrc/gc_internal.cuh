@@ -61,7 +61,7 @@ struct gc_ctx {
     int block_bitmap = 1;
     int long_seg = 48;
     int block_batch = 32;
-    int sup_uw = 0;
+    int sup_skip = 0;
     int huge_max = 8192;   // class 3: largest d+ in the 16384-slot shared hash (GC_OPT_HUGE_MAX)
 
     // raw input (a1)

@@ -48,6 +48,9 @@ constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not
 constexpr int kTS3 = 16384;    // huge-head hash slots (d+ <= kTS3/2 by default)
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
+#ifndef GC_VW_GLOBAL
+#define GC_VW_GLOBAL 0                      // 1: heavy-head support credits (v,w) by global atomics (measured slower)
+#endif
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
 // tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
@@ -182,8 +185,8 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                     const int hd = probe.loc((uint32_t)w);        // located once
                     if (inr && hd >= 0) {
                         ++seg_hits;
-                        probe.credit(hd, sup);                    // role (v,w)
-                        if (uw == 0) atomicAdd(sup + q, 1u);      // role (u,w)
+                        if (!(uw & 2)) probe.credit(hd, sup);     // role (v,w)
+                        if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
                     }
                 }
             };
@@ -209,7 +212,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             if (SUP) {
                 const uint32_t tot_hits = __reduce_add_sync(0xffffffffu, seg_hits);
                 const int ps = __shfl_sync(0xffffffffu, p, s);
-                if (lane == 0 && tot_hits) atomicAdd(sup + ps, tot_hits);   // role (u,v)
+                if (lane == 0 && tot_hits && !(uw & 4)) atomicAdd(sup + ps, tot_hits);   // role (u,v)
             }
         }
         if (len >= long_seg) len = 0;
@@ -243,15 +246,15 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                     if (slot >= 0) {
                         hit = true;
                         ++hits;
-                        probe.credit(slot, sup);       // role (v,w)
-                        if (uw == 0) atomicAdd(sup + q, 1u);   // role (u,w)
+                        if (!(uw & 2)) probe.credit(slot, sup);   // role (v,w)
+                        if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
                     }
                 }
             }
             if (SUP) {
                 // role (u,v): lanes of one segment are contiguous; one atomic per segment
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
-                if (hit) {
+                if (hit && !(uw & 4)) {
                     const unsigned grp = __match_any_sync(hm, s);
                     if (lane == __ffs(grp) - 1) atomicAdd(sup + ps, (uint32_t)__popc(grp));
                 }
@@ -281,8 +284,11 @@ struct SmemHash {
         }
     }
     __device__ __forceinline__ int loc(uint32_t w) const { return find(w); }
+    uint32_t* gsup = nullptr;   // non-null: credit (v,w) straight into the global row of v
     __device__ __forceinline__ void credit(int slot, uint32_t*) const {
-        if (SUP) atomicAdd(cnt + slot, 1u);
+        if (!SUP) return;
+        if (gsup) atomicAdd(gsup + vals[slot], 1u);
+        else atomicAdd(cnt + slot, 1u);
     }
     __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
@@ -304,7 +310,7 @@ struct KArgs {
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
     int long_seg;               // suffix length threshold of the warp-vector path
     int batch;                  // heavy-head kernel: consecutive tasks per batch
-    int uw;                     // (u,w)-role crediting mode (GC_OPT_SUP_UW)
+    int uw;                     // diagnostics: support roles skipped (GC_OPT_SUP_SKIP mask)
     int huge_max;               // class 3: largest d+ held in the shared hash
 };
 
@@ -446,7 +452,11 @@ struct GlobalProbe {
 };
 
 template <bool SUP, bool HUGE>
-__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArgs a) {
+__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) : 6)) k_tc_block(KArgs a) {
+    // kVWG: the heavy-head support kernel credits the (v,w) role with global
+    // atomics into v's row instead of shared counters, which frees 16 KB of
+    // shared memory per block (5 instead of 4 resident blocks per SM)
+    constexpr bool kVWG = SUP && !HUGE && GC_VW_GLOBAL;
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
@@ -478,7 +488,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArg
     uint32_t span = 0;
     bool use_bm = false, use_gp = false;   // use_gp: N+(v) too large for the table, search it in global memory
     auto teardown = [&](bool clear) {
-        if (SUP && !use_gp) {
+        if (SUP && !kVWG && !use_gp) {
             if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x)
                     if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArg
                 // nothing to stage
             } else if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x) {
-                    if (SUP) bcnt[j] = 0u;
+                    if (SUP && !kVWG) bcnt[j] = 0u;
                     const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
                     atomicOr(bits + (x >> 5), 1u << (x & 31));
                     if (SUP) {
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArg
                 ts = 1 << lg;
                 for (int j = threadIdx.x; j < ts; j += blockDim.x) {
                     keys[j] = kEmpty;
-                    if (SUP) hcnt[j] = 0;
+                    if (SUP && !kVWG) hcnt[j] = 0;
                 }
                 __syncthreads();
                 for (int j = threadIdx.x; j < d; j += blockDim.x) {
@@ -556,11 +566,11 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArg
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, seg, G, lane, a.long_seg, a.uw);
             } else if (use_bm) {
-                SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u, span};
+                SmemBitmap<SUP> B{bits, pre, kVWG ? a.sup + r0 : bcnt, (uint32_t)v + 1u, span};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, seg, B, lane, a.long_seg, a.uw);
             } else {
-                SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
+                SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1), kVWG ? a.sup + r0 : nullptr};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, seg, H, lane, a.long_seg, a.uw);
             }
@@ -696,7 +706,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.bm_bits = bm_bits_of(c);
     a.long_seg = c->long_seg;
     a.batch = c->block_batch;
-    a.uw = c->sup_uw;
+    a.uw = c->sup_skip;
     a.huge_max = c->huge_max;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
     // classes 3 and 2 first (heaviest tasks), then 1, 0
@@ -719,7 +729,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         a.next = next + 2;
-        const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
+        const size_t smem = (SUP ? kBWS + kBW / 4 + (GC_VW_GLOBAL ? 0 : kD2) : kBWS) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
             GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

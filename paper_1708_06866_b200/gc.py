@@ -36,7 +36,7 @@ GC_OPT_TIMING = 3
 GC_OPT_BLOCK_BITMAP = 4
 GC_OPT_LONG_SEG = 5
 GC_OPT_BLOCK_BATCH = 6
-GC_OPT_SUP_UW = 7
+GC_OPT_SUP_SKIP = 7
 GC_OPT_PEEL_PART = 8
 GC_OPT_HUGE_MAX = 9
 GC_OPT_COMPACT = 10
