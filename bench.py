@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--ktruss-k", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=1 << 15, help="edges in the oracle's support sample")
+    p.add_argument("--cpu-sample", type=int, default=1 << 20, help="edges in the oracle's support sample")
     return p.parse_args()
 
 
@@ -254,18 +254,32 @@ def main():
     value = m / (ms_per_step / 1e3)
     st = ctx.stats()
 
-    # ---- roofline of the dominant kernel: the TC intersection pass
+    # ---- roofline of the dominant kernel: the support intersection pass (two of
+    # the step's four calls run it: gc_edge_support and gc_ktruss), TC pass beside it
     peak, peak_src = hbm_peak()
-    b_alg = algorithmic_bytes_tc(st)
-    tck = float(np.mean(phase["tc_kernel_ms"]))
-    achieved = b_alg / (tck / 1e3) / 1e9 if tck > 0 else None
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "tc_ncu_summary.json")
-    if os.path.exists(prof):
+    b_tc = algorithmic_bytes_tc(st)
+    b_sup = b_tc + 4 * st["m"]                     # B_support = B_TC + 4m
+    ncu = {}
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof) and cfg.name == "C4":
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            ncu = json.load(open(prof))
         except Exception:
-            traffic = None
+            ncu = {}
+
+    def roof(kernel_ms, b_alg, key, label):
+        achieved = b_alg / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": ncu.get(key, {}).get("dram_bytes_per_launch"),
+                "kernel": label, "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms, "peak_source": peak_src}
+
+    sup_ms = float(np.mean(phase["support_kernel_ms"]))
+    tck = float(np.mean(phase["tc_kernel_ms"]))
+    roofline = roof(sup_ms, b_sup, "support",
+                    "support intersection pass (k_tc_* class kernels with SUP=1, one launch per class; "
+                    "run by gc_edge_support and again inside gc_ktruss)")
+    roofline_tc = roof(tck, b_tc, "tc", "triangle-count intersection pass (k_tc_* class kernels, SUP=0)")
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -313,10 +327,8 @@ def main():
                        "step": f"build_csr + triangle_count + edge_support + ktruss(k={k})",
                        "l2": "no flush: every input (raw list 2.1 GB, oriented CSR 1 GB) exceeds the 126 MB L2",
                        "parallelism": f"replicated graph, {world}-way balanced 1D intersection split"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "TC intersection pass (k_tc_* class kernels, one launch per class)",
-                         "algorithmic_bytes": b_alg, "kernel_ms": tck, "peak_source": peak_src},
+            "roofline": roofline,
+            "roofline_tc": roofline_tc,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -175,25 +175,42 @@ __global__ void k_alive_list(const uint8_t* __restrict__ alive, int64_t m, int32
 }
 
 // X = {alive e : S(e) < thr}, over the live-edge list (list == nullptr: all e < m)
-__global__ void k_frontier_scan(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive,
+// An edge below the threshold with S(e) = 0 lies in no live triangle, so it
+// is removed on the spot (nothing to destroy, nobody sees it in this round);
+// the others go to the frontier list for the peel kernel.
+__global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restrict__ alive,
                                 const int32_t* __restrict__ list, int64_t len, uint32_t thr,
                                 int32_t* __restrict__ rem, int32_t round, int32_t* __restrict__ front,
-                                int* __restrict__ count) {
+                                int* __restrict__ count, int32_t* __restrict__ tau, int32_t level,
+                                unsigned long long* __restrict__ zero_removed) {
+    const int lane = threadIdx.x & 31;
+    unsigned zeros = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = list ? (int64_t)list[i] : i;
-        bool in = alive[e] && S[e] < thr;
+        bool in = false;
+        if (alive[e]) {
+            const uint32_t se = S[e];
+            if (se == 0 && thr > 0) {
+                alive[e] = 0;
+                if (tau) tau[e] = level;
+                ++zeros;
+            } else {
+                in = se < thr;
+            }
+        }
         unsigned ballot = __ballot_sync(__activemask(), in);
         if (in) {
             rem[e] = round;
             // warp-aggregated append
             int leader = __ffs(ballot) - 1;
-            int lane = threadIdx.x & 31;
             int base = 0;
             if (lane == leader) base = atomicAdd(count, __popc(ballot));
             base = __shfl_sync(ballot, base, leader);
             front[base + __popc(ballot & ((1u << lane) - 1))] = (int32_t)e;
         }
     }
+    zeros = __reduce_add_sync(0xffffffffu, zeros);
+    if (lane == 0 && zeros) atomicAdd(zero_removed, (unsigned long long)zeros);
 }
 
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t lo, int64_t hi, int32_t x) {
@@ -458,12 +475,21 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     const int32_t* list = c->alist_n >= 0 ? c->alist.as<int32_t>() : nullptr;
     const int64_t len = c->alist_n >= 0 ? c->alist_n : m;
     GC_TRY(record(c, 10));
+    unsigned long long* zrem = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 240);
+    GC_CUDA(c, cudaMemsetAsync(zrem, 0, 8, c->stream));
     GC_LAUNCH(c, k_frontier_scan, grid_for(len), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), list,
-              len, thr, c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt);
+              len, thr, c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt,
+              level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem);
     GC_TRY(record(c, 11));
     GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_CUDA(c, cudaMemcpyAsync(h + 2, zrem, 8, cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
     c->stats.scan_ms += elapsed(c, 10, 11);
+    {
+        const int64_t z = *reinterpret_cast<int64_t*>(h + 2);   // removed on the spot (S = 0)
+        *removed += z;
+        c->m_alive_h -= z;
+    }
     int nf = h[0];
     int32_t* cur = c->front_a.as<int32_t>();
     int32_t* nxt = c->front_b.as<int32_t>();
