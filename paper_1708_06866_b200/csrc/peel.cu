@@ -22,6 +22,7 @@
 // continue from the previous k's survivors; edges removed at level k get
 // trussness k-1.
 #include <algorithm>
+#include <cstring>
 
 #include "gc_internal.cuh"
 
@@ -267,6 +268,7 @@ __device__ __forceinline__ void destroy(const Pol& pol, int e, int f, int g) {
 struct PeelArgs {
     const int32_t* front;
     int nfront;
+    const int* nfront_dev;  // non-null: the frontier size is read on the device (rounds enqueued ahead)
     const int32_t* dag_src;
     const int32_t* dag_col;
     const int64_t* sym_ptr;
@@ -288,7 +290,8 @@ template <class Pol>
 __global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < A.nfront; wi += warps) {
+    const int nfront = A.nfront_dev ? *A.nfront_dev : A.nfront;
+    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
         const int e = A.front[wi];
         const uint32_t live = pol.live(e);
         if (live == 0) continue;                 // no live triangle (the whole k = 3 peel)
@@ -375,6 +378,23 @@ __global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, ui
     }
 }
 
+// k_finish_round for a frontier whose size is on the device; also counts the
+// removed edges and the non-empty rounds
+__global__ void k_finish_round_dev(const int32_t* __restrict__ front, const int* __restrict__ nfront_dev,
+                                   uint8_t* __restrict__ alive, int32_t* __restrict__ tau, int32_t level,
+                                   unsigned long long* __restrict__ acc) {
+    const int nfront = *nfront_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
+        int e = front[i];
+        alive[e] = 0;
+        if (tau) tau[e] = level;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && nfront > 0) {
+        acc[0] += (unsigned long long)nfront;
+        acc[1] += 1ULL;
+    }
+}
+
 __global__ void k_scatter_u8(const uint8_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
                              uint8_t* __restrict__ out) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
@@ -455,7 +475,7 @@ static int maybe_compact(gc_ctx* c) {
 // One peel round over the frontier list.
 template <class Pol>
 static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
-    PeelArgs A{front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(), c->sym_ptr.as<int64_t>(),
+    PeelArgs A{front, nf, nullptr, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(), c->sym_ptr.as<int64_t>(),
                c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
                c->alive.as<uint8_t>()};
     const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
@@ -491,31 +511,48 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         c->m_alive_h -= z;
     }
     int nf = h[0];
-    int32_t* cur = c->front_a.as<int32_t>();
-    int32_t* nxt = c->front_b.as<int32_t>();
-    int* ncnt = cnt + 1;
+    // Rounds are enqueued in batches without a host round trip: each round's
+    // kernels read the frontier size on the device (an empty frontier makes a
+    // round a no-op), and the host looks at the next frontier size only after
+    // each batch (batch length 2, 4, ..., 16 rounds within a level).
+    int32_t* lists[2] = {c->front_a.as<int32_t>(), c->front_b.as<int32_t>()};
+    int* counts[2] = {cnt, cnt + 1};
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 256);   // removed, rounds
+    GC_CUDA(c, cudaMemsetAsync(acc, 0, 16, c->stream));
+    const int64_t alive0 = c->m_alive_h;
+    int cur = 0, batch = 2;
+    unsigned long long done[2] = {0, 0};
     while (nf > 0) {
-        GC_CUDA(c, cudaMemsetAsync(ncnt, 0, sizeof(int), c->stream));
         GC_TRY(record(c, 8));
-        PolicySingle pol{c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, nxt, ncnt};
-        GC_TRY(peel_round(c, cur, nf, pol));
+        for (int r = 0; r < batch; ++r) {
+            const int nxt = cur ^ 1;
+            GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
+            PolicySingle pol{c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, lists[nxt], counts[nxt]};
+            PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                       c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                       c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
+            GC_LAUNCH(c, k_peel<PolicySingle>, 148 * 8, 256, 0, A, pol);
+            GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
+                      level >= 0 ? c->tau.as<int32_t>() : nullptr, level, acc);
+            ++*round;
+            cur = nxt;
+        }
         GC_TRY(record(c, 9));
-        GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, cur, nf, c->alive.as<uint8_t>(),
-                  level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
-        GC_CUDA(c, cudaMemcpyAsync(h, ncnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_CUDA(c, cudaMemcpyAsync(h, counts[cur], sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_CUDA(c, cudaMemcpyAsync(h + 2, acc, 16, cudaMemcpyDeviceToHost, c->stream));
         GC_TRY(sync(c));
         c->stats.peel_kernel_ms += elapsed(c, 8, 9);
-        if (c->trace) fprintf(stderr, "peel-trace level %d round %d nf %d ms %.4f\n", level, *round, nf, elapsed(c, 8, 9));
-        *removed += nf;
-        c->m_alive_h -= nf;
-        ++*round;
-        c->stats.peel_rounds++;
+        memcpy(done, h + 2, 16);
+        if (c->trace)
+            fprintf(stderr, "peel-trace level %d batch %d rounds %llu removed %llu ms %.4f\n", level, batch, done[1],
+                    done[0], elapsed(c, 8, 9));
+        c->m_alive_h = alive0 - (int64_t)done[0];
         nf = h[0];
-        GC_TRY(maybe_compact(c));
-        int32_t* t = cur;
-        cur = nxt;
-        nxt = t;
+        if (nf > 0) GC_TRY(maybe_compact(c));
+        batch = std::min(batch * 2, 16);
     }
+    *removed += (int64_t)done[0];
+    c->stats.peel_rounds += (int64_t)done[1];
     ++*round;   // fresh stamp for the next level's scan
     return GC_OK;
 }
