@@ -192,9 +192,14 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             };
             // a vector wholly inside [b, e) needs no per-element bounds checks
             auto visit4 = [&](int q0, const int4& V) {
-                if (!SUP && q0 >= b && q0 + 4 <= e) {
-                    seg_hits += probe.hit((uint32_t)V.x) + probe.hit((uint32_t)V.y) + probe.hit((uint32_t)V.z) +
-                                probe.hit((uint32_t)V.w);
+                if (!SUP) {
+                    // count: all four probes in every lane, then a mask of the
+                    // positions inside [b, e) (no divergent path at the segment ends)
+                    const int klo = max(b - q0, 0), khi = min(e - q0, 4);
+                    const uint32_t in4 = khi > klo ? (1u << khi) - (1u << klo) : 0u;
+                    const uint32_t h4 = probe.hit((uint32_t)V.x) | (probe.hit((uint32_t)V.y) << 1) |
+                                        (probe.hit((uint32_t)V.z) << 2) | (probe.hit((uint32_t)V.w) << 3);
+                    seg_hits += __popc(h4 & in4);
                 } else {
                     visit(q0, V.x); visit(q0 + 1, V.y); visit(q0 + 2, V.z); visit(q0 + 3, V.w);
                 }

@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:warnings -k "not c5 and not c4" 2>&1 | tail -2
-for C in C3 C4 C4 C5; do timeout 600 python scripts/run_decomp.py --config $C --ks 3,8 2>&1 | tail -3; done
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:warnings -k "forced or heavy or huge or chunk or c3 or loopback or c1 or golden or clique" 2>&1 | tail -2
+timeout 600 python scripts/tune.py C4 "long_seg=48" "long_seg=32" "long_seg=24" 2>&1 | tail -3
