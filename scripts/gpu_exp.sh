@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:warnings -k "forced or heavy or huge or chunk or c3 or loopback or c1 or golden or clique" 2>&1 | tail -2
-timeout 600 python scripts/tune.py C4 "long_seg=48" "long_seg=32" "long_seg=24" 2>&1 | tail -3
+for M in 4 16 64; do echo "min=$M"; GC_LIB_PATH=exp/libgc_g$M.so timeout 900 python scripts/run_decomp.py --config C4 --ks 8 2>&1 | tail -2; done
+echo "group=0"; timeout 900 python scripts/run_decomp.py --config C4 --ks 8 --group 0 2>&1 | tail -2

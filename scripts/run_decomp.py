@@ -12,6 +12,7 @@ p.add_argument("--part", type=int, default=0)
 p.add_argument("--loop", type=int, default=0)
 p.add_argument("--tc", type=int, default=0)
 p.add_argument("--compact", type=int, default=-1)
+p.add_argument("--group", type=int, default=-1)
 p.add_argument("--no-decomp", action="store_true")
 a = p.parse_args()
 t0 = time.time()
@@ -20,6 +21,8 @@ print(f"gen {time.time()-t0:.1f}s nnz={u.size}", flush=True)
 ctx = gc.Context(0, torch.cuda.current_stream())
 if a.loop:
     ctx.comm_init_loopback(a.loop)
+if a.group >= 0:
+    ctx.set_option(gc.GC_OPT_GROUP_PEEL, a.group)
 if a.compact >= 0:
     ctx.set_option(gc.GC_OPT_COMPACT, a.compact)
 if a.part:
