@@ -113,6 +113,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class EnergyMeter:
+    """NVML total-energy counter (mJ) read around the timed region: the paper's
+    energy and rate-per-energy metrics (reading A20: joules, and
+    edges/s/W = rate / mean power).  None when NVML is unavailable."""
+
+    def __init__(self, index: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)) / 1e3   # J
+        except Exception:
+            return None
+
+
 def algorithmic_bytes_tc(st):
     """B_TC = s_o(n+1) + (4 + 2 s_o) m + 4 min(Q_out, Q_in), s_o = 8 (int64 offsets)."""
     s_o = 8
@@ -235,15 +260,18 @@ def main():
         torch.cuda.synchronize()
 
     ctx.reset_stats()
+    meter = EnergyMeter(local)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        j0 = meter.read()
         ev0.record(stream)
         for _ in range(args.steps):
             step(record=True)
         ev1.record(stream)
         barrier()
+        j1 = meter.read()
     launches = ctx.stats()["launches"]
     t_ms = ev0.elapsed_time(ev1)
     if world > 1:
@@ -252,6 +280,12 @@ def main():
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
     value = m / (ms_per_step / 1e3)
+    energy = None
+    if j0 is not None and j1 is not None and j1 > j0:
+        jps = (j1 - j0) / args.steps                      # this GPU's joules per step
+        watts = jps / (ms_per_step / 1e3)
+        energy = {"joules_per_step_per_gpu": jps, "mean_power_w_per_gpu": watts,
+                  "edges_per_s_per_w": value / (watts * world), "source": "NVML total energy counter"}
     st = ctx.stats()
 
     # ---- roofline of the dominant kernel: the support intersection pass (two of
@@ -334,6 +368,7 @@ def main():
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk.summary(),
+            "energy": energy,
             "phase_ms": mean,
             "triangles": results.get("T"),
             "ktruss_edges": results.get("ktruss_edges"),

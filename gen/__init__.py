@@ -98,7 +98,7 @@ def vertex_perm(seed: int, s: int, x: int) -> int:
 @dataclass(frozen=True)
 class Config:
     name: str
-    kind: str            # "rmat" | "er"
+    kind: str            # "rmat" | "er" | "king" (n = M, the grid side)
     scale: int = 0
     edge_factor: int = 16
     a: float = 0.57
@@ -114,6 +114,8 @@ class Config:
             return rmat(self.scale, self.edge_factor, self.a, self.b, self.c, self.seed, True, nthreads)
         if self.kind == "er":
             return erdos_renyi(self.n, self.mean_degree, self.seed, nthreads)
+        if self.kind == "king":
+            return king_grid(self.n)
         raise ValueError(self.kind)
 
 
@@ -125,4 +127,7 @@ CONFIGS = {
     "C4": Config("C4", "rmat", scale=24, seed=4, desc="R-MAT s24 ef16 (0.57,0.19,0.19,0.05) seed 4"),
     "C5": Config("C5", "rmat", scale=26, a=0.65, b=0.15, c=0.15, seed=5,
                  desc="R-MAT s26 ef16 skewed (0.65,0.15,0.15,0.05) seed 5"),
+    # the paper's own synthetic graphs, Table II: M x M king grids, M = 2^12, 2^13
+    "K12": Config("K12", "king", n=4096, desc="king grid M=4096 (Table II row 12: 67,084,290 edges)"),
+    "K13": Config("K13", "king", n=8192, desc="king grid M=8192 (Table II row 13: 268,386,306 edges)"),
 }

@@ -16,5 +16,6 @@ from .gc import (  # noqa: F401
     load_library,
     nccl_unique_id,
 )
+from .io import read_mmio, read_tsv, write_mmio, write_tsv  # noqa: F401
 
 __all__ = ["Context", "GcError", "init_distributed", "load_library", "nccl_unique_id", "EXPORTS"]

@@ -532,3 +532,40 @@ def test_hypothesis_oracle(raw):
         for k in (3, 4):
             want = {idx[(min(a, b), max(a, b))] for a, b in nx.k_truss(G, k).edges()}
             assert set(np.flatnonzero(tau >= k).tolist()) == want
+
+
+# ------------------------------------------------------- file formats --
+def test_tsv_and_mmio_round_trip(tmp_path):
+    """Graph Challenge TSV triples and MMIO coordinate files, 1-based on disk,
+    0-based pairs in memory; the oracle sees the same graph either way."""
+    from paper_1708_06866_b200 import io as gio
+    u, v = gen.rmat(9, 8, seed=11)
+    p = str(tmp_path / "g.tsv")
+    gio.write_tsv(p, u, v)
+    first = open(p).readline().split("\t")
+    assert int(first[0]) == u[0] + 1 and int(first[1]) == v[0] + 1 and first[2].strip() == "1"
+    ru, rv = gio.read_tsv(p)
+    assert np.array_equal(ru, u) and np.array_equal(rv, v)
+    q = str(tmp_path / "g.mtx")
+    gio.write_mmio(q, u, v)
+    mu, mv = gio.read_mmio(q)
+    assert np.array_equal(mu, u) and np.array_equal(mv, v)
+    assert oracle.OracleGraph(ru, rv).triangle_count() == oracle.OracleGraph(u, v).triangle_count()
+    with open(str(tmp_path / "bad.tsv"), "w") as f:
+        f.write("0\t3\t1\n")
+    with pytest.raises(ValueError):
+        gio.read_tsv(str(tmp_path / "bad.tsv"))
+
+
+def test_king_grid_configs_match_table2():
+    """K12 / K13 bench workloads are Table II rows 12 and 13."""
+    rows = {}
+    for line in open(os.path.join(GOLDEN, "table2_king_grid.tsv")):
+        if line.startswith("#") or not line.strip():
+            continue
+        nn, nodes, edges, tri = (int(x) for x in line.split())
+        rows[nn] = (nodes, edges, tri)
+    for name, nn in (("K12", 12), ("K13", 13)):
+        cfg = gen.CONFIGS[name]
+        assert cfg.n == 2 ** nn and cfg.n ** 2 == rows[nn][0]
+        assert 2 * (cfg.n - 1) * (2 * cfg.n - 1) == rows[nn][1]

@@ -179,6 +179,41 @@ def test_king_grid(ctx):
         assert ctx.triangle_count() == 4 * (M - 1) ** 2
 
 
+@pytest.mark.parametrize("name", ["K12", "K13"])
+def test_king_grid_table2_full_size(gcmod, name):
+    """The paper's own synthetic graphs at Table II's largest sizes,
+    against closed forms rather than the oracle: n = M^2, m = 2(M-1)(2M-1)
+    (Table II), T = 4(M-1)^2 (= Table II / 2, reading A9); per edge, a
+    horizontal or vertical edge has support 4 (2 on the border row / column it
+    runs along), a diagonal edge 2; every triangle uses a diagonal, so the
+    4-truss is the whole graph, the 5-truss is empty and every trussness is 4."""
+    import torch
+    M = gen.CONFIGS[name].n
+    u, v = gen.CONFIGS[name].generate()
+    c = gcmod.Context(0, torch.cuda.current_stream())
+    try:
+        c.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+        c.build_csr()
+        n, m = c.num_vertices(), c.num_edges()
+        T = c.triangle_count()
+        sup = c.edge_support()
+        cu, cv = c.get_edges()
+        m4 = c.ktruss(4)[1]
+        m5 = c.ktruss(5)[1]
+        tau, kmax = c.truss_decomposition()
+    finally:
+        c.close()
+    assert n == M * M and m == 2 * (M - 1) * (2 * M - 1) and T == 4 * (M - 1) ** 2
+    d = cv.astype(np.int64) - cu.astype(np.int64)
+    r, col = cu // M, cu % M
+    want = np.full(m, 2, np.uint32)
+    want[(d == 1) & (r > 0) & (r < M - 1)] = 4
+    want[(d == M) & (col > 0) & (col < M - 1)] = 4
+    assert np.all((d == 1) | (d == M) | (d == M - 1) | (d == M + 1))
+    assert np.array_equal(sup, want)
+    assert m4 == m and m5 == 0 and kmax == 4 and np.all(tau == 4)
+
+
 # ------------------------------------------------------------------ configs --
 def test_c1_full(ctx):
     u, v = gen.CONFIGS["C1"].generate()
