@@ -1,3 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:warnings -k "king" 2>&1 | tail -2
-timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo bench rc=$?; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); [print(k, d[k]) for k in ['value','ms_per_step','energy','phase_ms']]"
-timeout 900 python bench.py --config K13 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_k13.log 2>&1; echo bench rc=$?; tail -1 gpurun_out/bench_k13.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); [print(k, d[k]) for k in ['value','ms_per_step','energy','phase_ms','roofline']]"
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:warnings -k "forced or heavy or huge or chunk or c3 or c1 or golden or clique" 2>&1 | tail -2
+timeout 600 python scripts/tune.py C4 "sup_skip=0" "sup_skip=2" 2>&1 | tail -2
