@@ -14,15 +14,17 @@
 // Only the suffix of N+(u) past v can meet N+(v) (its entries all rank
 // above v), so the streamed volume is Σ_x C(d+(x), 2) wedges instead of the
 // full Σ d-·d+ (DESIGN.md "Kernels").  Per-edge support credits the three
-// edges of each triangle found:  (u,v) via a per-in-edge shared counter,
-// (v,w) via a per-hash-slot shared counter, (u,w) via one global atomic.
+// edges of each triangle found:  (u,v) by a warp reduction over the in-edge's
+// hits (one atomic per segment), (v,w) by a shared counter per element of
+// N+(v) flushed once per head, (u,w) by one global atomic.
 //
-// Task classes by d+(v): 0 warp task, 64-slot table; 1 warp task,
-// 512-slot table; 2 block task, 8192-slot table; 3 warp task, binary search
-// of N+(v) in global memory (d+(v) > 4096, rare).  Tasks are (v, in-edge
-// range) cut by an exclusive scan of a per-in-edge cost so every task holds
-// about task_chunk wedges; the same cut points give the multi-GPU 1D
-// partition.
+// Task classes by d+(v): 0 warp task, 64-slot hash; 1 warp task,
+// 512-slot hash; 2 block task, rank-window bitmap (or a 4096-slot hash);
+// 3 block task, 16384-slot hash (binary search of N+(v) in global memory only
+// past GC_OPT_HUGE_MAX).  Tasks are (v, in-edge range) cut by an exclusive
+// scan of a per-in-edge cost so every task holds about task_chunk wedges (8x
+// for block tasks); the same cut points give the multi-GPU 1D partition
+// (SURVEY §8(e)).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -48,9 +50,6 @@ constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not
 constexpr int kTS3 = 16384;    // huge-head hash slots (d+ <= kTS3/2 by default)
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
-#ifndef GC_VW_GLOBAL
-#define GC_VW_GLOBAL 0                      // 1: heavy-head support credits (v,w) by global atomics (measured slower)
-#endif
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
 // tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
@@ -148,7 +147,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                                                 const int64_t* __restrict__ in_cost,
                                                 const int64_t* __restrict__ dag_ptr,
                                                 const int32_t* __restrict__ dag_col, uint32_t* __restrict__ sup,
-                                                uint32_t* seg_cnt, Probe& probe, int lane, int long_seg, int uw) {
+                                                Probe& probe, int lane, int long_seg, int uw) {
     uint32_t hits = 0;
     for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
@@ -266,7 +265,6 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             }
         }
     }
-    (void)seg_cnt;
     return hits;
 }
 
@@ -289,11 +287,8 @@ struct SmemHash {
         }
     }
     __device__ __forceinline__ int loc(uint32_t w) const { return find(w); }
-    uint32_t* gsup = nullptr;   // non-null: credit (v,w) straight into the global row of v
     __device__ __forceinline__ void credit(int slot, uint32_t*) const {
-        if (!SUP) return;
-        if (gsup) atomicAdd(gsup + vals[slot], 1u);
-        else atomicAdd(cnt + slot, 1u);
+        if (SUP) atomicAdd(cnt + slot, 1u);
     }
     __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
@@ -311,7 +306,6 @@ struct KArgs {
     int parts, owner;           // skip tasks not owned by `owner` of `parts`
     uint32_t* sup;
     unsigned long long* count;
-    int* next;                  // dynamic task counter
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
     int long_seg;               // suffix length threshold of the warp-vector path
     int batch;                  // heavy-head kernel: consecutive tasks per batch
@@ -336,11 +330,10 @@ template <int TS, bool SUP>
 __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int per_warp = SUP ? (3 * TS + 32) : TS;
+    constexpr int per_warp = SUP ? 3 * TS : TS;
     uint32_t* keys = smem + warp * per_warp;
     int32_t* vals = reinterpret_cast<int32_t*>(keys + TS);
     uint32_t* cnt = keys + 2 * TS;
-    uint32_t* seg = keys + 3 * TS;
     constexpr int max_lg = __builtin_ctz(TS);
     uint32_t hits = 0;
     // static round-robin over tasks (every task's cost is bounded by the chunk)
@@ -368,7 +361,7 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
         __syncwarp();
         SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
         hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
-                                        seg, H, lane, a.long_seg, a.uw);
+                                        H, lane, a.long_seg, a.uw);
         if (SUP) {
             __syncwarp();
             for (int j = lane; j < ts; j += 32)
@@ -392,7 +385,6 @@ struct SmemBitmap {
     const uint16_t* pre;     // SUP: index in N+(v) of the first element of each 64-bit chunk
     uint32_t* cnt;           // SUP: (v,w)-role credits per index j
     uint32_t base;           // v + 1
-    uint32_t nbits;
     // membership only, branch-free: one LDS from the shared window (no
     // generic-pointer conversion).  Words past the head's span are zero and
     // word kBW-1 is a permanent zero sentinel, so clamping the word index is
@@ -457,15 +449,11 @@ struct GlobalProbe {
 };
 
 template <bool SUP, bool HUGE>
-__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) : 6)) k_tc_block(KArgs a) {
-    // kVWG: the heavy-head support kernel credits the (v,w) role with global
-    // atomics into v's row instead of shared counters, which frees 16 KB of
-    // shared memory per block (5 instead of 4 resident blocks per SM)
-    constexpr bool kVWG = SUP && !HUGE && GC_VW_GLOBAL;
+__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
-    // SUP: [kBW, kBW + kBW/2) u16 prefix | hash cnt ; then kD2 bitmap-mode cnt ; then seg
+    // SUP: [kBW, kBW + kBW/4) u16 prefix per 64-bit chunk | hash cnt ; then kD2 bitmap-mode cnt
     // HUGE (class 3): [0, kTS3) keys | [kTS3, 2 kTS3) vals | [2 kTS3, 3 kTS3) cnt (SUP only)
     constexpr int kTSH = HUGE ? kTS3 : kTS2;
     constexpr int kZero = HUGE ? kTS3 : kBWS;    // words kept zero between heads
@@ -475,7 +463,6 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) 
     uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);    // kBW/2 u16 = kBW/4 words
     uint32_t* hcnt = HUGE ? smem + 2 * kTS3 : smem + kBWS;        // hash mode: kTSH words
     uint32_t* bcnt = smem + kBWS + kBW / 4;                        // bitmap mode: kD2 words
-    uint32_t* seg = nullptr;                                       // (unused: (u,v) credits use match_any)
     static_assert(kTS2 <= kBW / 4 + kD2, "hash counters fit the SUP region");
     constexpr int max_lg = __builtin_ctz(kTSH);
     static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
@@ -493,7 +480,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) 
     uint32_t span = 0;
     bool use_bm = false, use_gp = false;   // use_gp: N+(v) too large for the table, search it in global memory
     auto teardown = [&](bool clear) {
-        if (SUP && !kVWG && !use_gp) {
+        if (SUP && !use_gp) {
             if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x)
                     if (bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
@@ -534,7 +521,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) 
                 // nothing to stage
             } else if (use_bm) {
                 for (int j = threadIdx.x; j < d; j += blockDim.x) {
-                    if (SUP && !kVWG) bcnt[j] = 0u;
+                    if (SUP) bcnt[j] = 0u;
                     const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
                     atomicOr(bits + (x >> 5), 1u << (x & 31));
                     if (SUP) {
@@ -548,7 +535,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) 
                 ts = 1 << lg;
                 for (int j = threadIdx.x; j < ts; j += blockDim.x) {
                     keys[j] = kEmpty;
-                    if (SUP && !kVWG) hcnt[j] = 0;
+                    if (SUP) hcnt[j] = 0;
                 }
                 __syncthreads();
                 for (int j = threadIdx.x; j < d; j += blockDim.x) {
@@ -569,15 +556,15 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? (GC_VW_GLOBAL ? 5 : 4) 
             if (use_gp) {
                 GlobalProbe G{a.dag_col + r0, d, r0};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, seg, G, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, G, lane, a.long_seg, a.uw);
             } else if (use_bm) {
-                SmemBitmap<SUP> B{bits, pre, kVWG ? a.sup + r0 : bcnt, (uint32_t)v + 1u, span};
+                SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, seg, B, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, B, lane, a.long_seg, a.uw);
             } else {
-                SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1), kVWG ? a.sup + r0 : nullptr};
+                SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
                 hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, seg, H, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, H, lane, a.long_seg, a.uw);
             }
         }
     }
@@ -694,8 +681,6 @@ int prepare_tasks(gc_ctx* c) {
 // Launch every class kernel for owner `owner` of `parts`.
 template <bool SUP>
 static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* count, uint32_t* sup) {
-    int* next = reinterpret_cast<int*>(c->scal.as<char>() + 64);
-    GC_CUDA(c, cudaMemsetAsync(next, 0, 4 * sizeof(int), c->stream));
     KArgs a{};
     a.in_pos = c->in_pos.as<int32_t>();
     a.in_src = c->in_src.as<int32_t>();
@@ -718,7 +703,6 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[3] > 0) {
         a.tasks = tasks + c->task_off[3];
         a.ntask = c->ntask[3];
-        a.next = next + 3;
         const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
@@ -733,8 +717,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[2] > 0) {
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
-        a.next = next + 2;
-        const size_t smem = (SUP ? kBWS + kBW / 4 + (GC_VW_GLOBAL ? 0 : kD2) : kBWS) * sizeof(uint32_t);
+        const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
         static bool attr_set[2] = {false, false};
         if (!attr_set[SUP]) {
             GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -748,8 +731,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
         a.ntask = c->ntask[1];
-        a.next = next + 1;
-        const size_t smem = kWarps * (SUP ? 3 * kTS1 + 32 : kTS1) * sizeof(uint32_t);
+        const size_t smem = kWarps * (SUP ? 3 * kTS1 : kTS1) * sizeof(uint32_t);
         static bool attr_set = false;
         if (!attr_set) {
             GC_CUDA(c, cudaFuncSetAttribute(k_tc_warp<kTS1, SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -763,8 +745,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[0] > 0) {
         a.tasks = tasks + c->task_off[0];
         a.ntask = c->ntask[0];
-        a.next = next + 0;
-        const size_t smem = kWarps * (SUP ? 3 * kTS0 + 32 : kTS0) * sizeof(uint32_t);
+        const size_t smem = kWarps * (SUP ? 3 * kTS0 : kTS0) * sizeof(uint32_t);
         static int grid = 0;
         if (!grid) grid = occupancy_grid(k_tc_warp<kTS0, SUP>, smem);
         GC_LAUNCH(c, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
