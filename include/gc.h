@@ -183,6 +183,9 @@ typedef enum gc_option {
     GC_OPT_COMPACT = 10,      /* peeler: drop dead entries from the adjacency rows each
                                  time the live edge count falls to 1/value of the last
                                  compaction (default 2; 0 or 1: never; testing) */
+    GC_OPT_OVERLAP = 13,      /* 1: the warp-task intersection kernels run on a library
+                                 side stream that overlaps the block-task kernels and is
+                                 joined before the call returns (default); 0: one stream */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

@@ -162,6 +162,10 @@ int gc_create(gc_ctx** out, int device, void* cuda_stream) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     for (auto& ev : c->ev) cudaEventCreate(&ev);
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        c->side = nullptr;          // no overlap: everything stays on the context stream
     cudaGetLastError();
     *out = c;
     return GC_OK;
@@ -183,6 +187,9 @@ int gc_destroy(gc_ctx* c) {
     if (c->hpin) cudaFreeHost(c->hpin);
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     cudaGetLastError();
     delete c;
@@ -384,6 +391,9 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
         case GC_OPT_COMPACT:
             if (value < 0 || value > 1024) return fail(c, GC_ERR_INVALID, "compaction divisor must be 0..1024");
             c->compact_div = (int)value;
+            return GC_OK;
+        case GC_OPT_OVERLAP:
+            c->overlap = value ? 1 : 0;
             return GC_OK;
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;

@@ -44,12 +44,23 @@ struct Buf {
         if (_e != cudaSuccess) return gcx::cuda_fail((ctx), _e, #kernel, __FILE__, __LINE__); \
     } while (0)
 
+#define GC_LAUNCH_S(ctx, strm, kernel, grid, block, smem, ...)                          \
+    do {                                                                                \
+        (ctx)->stats.launches++;                                                        \
+        kernel<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);                       \
+        cudaError_t _e = cudaGetLastError();                                            \
+        if (_e != cudaSuccess) return gcx::cuda_fail((ctx), _e, #kernel, __FILE__, __LINE__); \
+    } while (0)
+
 }  // namespace gcx
 
 struct gc_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t side = nullptr;     // library-owned side stream (warp-task classes overlap the block kernels)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int overlap = 1;                 // GC_OPT_OVERLAP
     std::string err;
     bool poisoned = false;
     int state = 0;  // 0 created, 1 edges loaded, 2 graph built

@@ -699,6 +699,16 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.uw = c->sup_skip;
     a.huge_max = c->huge_max;
     const uint64_t* tasks = c->task_i0.as<uint64_t>();
+    // The warp-task classes (1, 0) run on a side stream forked from the
+    // context stream, so they fill the SMs the block-task kernels (3, 2)
+    // leave idle at their tails; the context stream joins it before return.
+    const bool fork = c->overlap && c->side && (c->ntask[3] > 0 || c->ntask[2] > 0) &&
+                      (c->ntask[1] > 0 || c->ntask[0] > 0);
+    cudaStream_t ws = fork ? c->side : c->stream;
+    if (fork) {
+        GC_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
+        GC_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    }
     // classes 3 and 2 first (heaviest tasks), then 1, 0
     if (c->ntask[3] > 0) {
         a.tasks = tasks + c->task_off[3];
@@ -740,7 +750,8 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         }
         static int grid = 0;
         if (!grid) grid = occupancy_grid(k_tc_warp<kTS1, SUP>, smem);
-        GC_LAUNCH(c, (k_tc_warp<kTS1, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
+        GC_LAUNCH_S(c, ws, (k_tc_warp<kTS1, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256,
+                    smem, a);
     }
     if (c->ntask[0] > 0) {
         a.tasks = tasks + c->task_off[0];
@@ -748,7 +759,12 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         const size_t smem = kWarps * (SUP ? 3 * kTS0 : kTS0) * sizeof(uint32_t);
         static int grid = 0;
         if (!grid) grid = occupancy_grid(k_tc_warp<kTS0, SUP>, smem);
-        GC_LAUNCH(c, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256, smem, a);
+        GC_LAUNCH_S(c, ws, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256,
+                    smem, a);
+    }
+    if (fork) {
+        GC_CUDA(c, cudaEventRecord(c->ev_join, c->side));
+        GC_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     return GC_OK;
 }
