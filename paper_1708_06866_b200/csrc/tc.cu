@@ -40,7 +40,10 @@ namespace {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kOvh = 2;                     // per in-edge overhead in the cost model
-constexpr int kD0 = 32, kD1 = 256, kD2 = 4096;
+#ifndef GC_KD1
+#define GC_KD1 128
+#endif
+constexpr int kD0 = 32, kD1 = GC_KD1, kD2 = 4096;   // class bounds on d+(v)
 constexpr int kTS0 = 64, kTS1 = 512;
 constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB); the last one is a zero
 constexpr int kBWS = kBW;      // sentinel, so heads spanning <= 32*(kBW-1) ranks fit
