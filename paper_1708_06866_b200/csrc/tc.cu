@@ -43,8 +43,13 @@ constexpr int kOvh = 2;                     // per in-edge overhead in the cost 
 #ifndef GC_KD1
 #define GC_KD1 128
 #endif
-constexpr int kD0 = 32, kD1 = GC_KD1, kD2 = 4096;   // class bounds on d+(v)
-constexpr int kTS0 = 64, kTS1 = 512;
+constexpr int kD0 = 8, kD1 = GC_KD1, kD2 = 4096;    // class bounds on d+(v)
+constexpr int kTS1 = 512;
+constexpr int64_t kTinyChunk = 256;   // class-0 task budget: one task per lane, keep lanes even
+#ifndef GC_TINY_IN
+#define GC_TINY_IN 64
+#endif
+constexpr int64_t kTinyIn = GC_TINY_IN;   // class 0 also needs at most this many in-edges
 constexpr int kBW = 8192;      // heavy-head bitmap words (32 KB); the last one is a zero
 constexpr int kBWS = kBW;      // sentinel, so heads spanning <= 32*(kBW-1) ranks fit
 
@@ -60,10 +65,14 @@ constexpr int kWarps = 8;                   // 256 threads per block
 // per SM; d+ above the huge-hash limit searches N+(v) in global memory).
 // force raises the class (testing).
 __device__ __forceinline__ int head_class(const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col,
-                                          int v, int force, uint32_t bm_bits) {
+                                          const int64_t* __restrict__ in_ptr, int v, int force, uint32_t bm_bits) {
     const int64_t r0 = dag_ptr[v];
     const int64_t d = dag_ptr[v + 1] - r0;
-    int c = d <= kD0 ? 0 : d <= kD1 ? 1 : 2;
+    // lane tasks only for tiny heads with few in-edges: a hub with a short
+    // N+(v) but many in-neighbours would serialise long suffixes in lanes
+    // and pile its (v,w) credits on a handful of global counters
+    const bool tiny = d <= kD0 && in_ptr[v + 1] - in_ptr[v] <= kTinyIn;
+    int c = tiny ? 0 : d <= kD1 ? 1 : 2;
     if (c < force) c = force;
     if (c == 2) {
         const uint32_t span = d > 0 ? (uint32_t)dag_col[r0 + d - 1] - (uint32_t)v : 0u;
@@ -108,7 +117,8 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
         uint8_t f = 0;
         if (dv > 0 && pref[e] > pref[s]) {
             // block-class tasks get 8x the budget (8 warps share one table)
-            const int64_t ch = head_class(dag_ptr, dag_col, v, force, bm_bits) >= 2 ? chunk * kWarps : chunk;
+            const int cl = head_class(dag_ptr, dag_col, in_ptr, v, force, bm_bits);
+            const int64_t ch = cl >= 2 ? chunk * kWarps : cl == 0 ? min(chunk, kTinyChunk) : chunk;
             if (i == s) f = 1;
             else if (pref[i] / ch != pref[i - 1] / ch) f = 1;
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
@@ -127,7 +137,7 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
         int v = in_dst[i0];
         int64_t nxt = (j + 1 < ntask) ? (int64_t)sel[j + 1] : m;
         int64_t i1 = min(nxt, in_ptr[v + 1]);
-        int k = head_class(dag_ptr, dag_col, v, force, bm_bits);
+        int k = head_class(dag_ptr, dag_col, in_ptr, v, force, bm_bits);
         cls[j] = (uint32_t)k;
         packed[j] = (uint64_t)(uint32_t)i0 | ((uint64_t)(uint32_t)i1 << 32);
         atomicAdd(hist + k, 1ULL);
@@ -328,7 +338,55 @@ __device__ __forceinline__ void add_count(unsigned long long* count, uint32_t hi
     if (lane == 0 && h) atomicAdd(count, h);
 }
 
-// ------------------------------------------------- warp-task kernel (0, 1) --
+// ------------------------------------------------ lane-task kernel (0) --
+// Tiny heads (d+(v) <= 8), the bulk of the heads of uniform-degree graphs
+// (king grids, ER) and of the R-MAT periphery: one task per lane, N+(v) in
+// eight registers, each suffix element compared against all of them.  A
+// warp thus keeps 32 independent tasks' loads in flight instead of
+// building a shared table per head.  Suffix scans stop past max N+(v).
+template <bool SUP>
+__global__ void __launch_bounds__(256) k_tc_tiny(KArgs a) {
+    const int lane = threadIdx.x & 31;
+    uint32_t hits = 0;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.ntask; t += nt) {
+        const uint64_t pk = a.tasks[t];
+        const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
+        if (!owned(a, i0)) continue;
+        const int v = __ldg(a.in_dst + i0);
+        const int64_t r0 = __ldg(a.dag_ptr + v);
+        const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
+        int32_t sv[kD0];
+#pragma unroll
+        for (int k = 0; k < kD0; ++k) sv[k] = k < d ? __ldg(a.dag_col + r0 + k) : -1;
+        const int32_t vmax = sv[0] < 0 ? -1 : __ldg(a.dag_col + r0 + d - 1);
+        for (int i = i0; i < i1; ++i) {
+            const int p = __ldg(a.in_pos + i);
+            const int u = __ldg(a.in_src + i);
+            const int64_t e = __ldg(a.dag_ptr + u + 1);
+            uint32_t seg = 0;
+            for (int64_t q = p + 1; q < e; ++q) {
+                const int32_t w = __ldg(a.dag_col + q);
+                if (w > vmax) break;                       // rows ascend: nothing further can match
+                uint32_t mk = 0;
+#pragma unroll
+                for (int k = 0; k < kD0; ++k) mk |= (uint32_t)(w == sv[k]) << k;
+                if (mk) {
+                    ++seg;
+                    if (SUP) {
+                        if (!(a.uw & 1)) atomicAdd(a.sup + q, 1u);                     // role (u,w)
+                        if (!(a.uw & 2)) atomicAdd(a.sup + r0 + (__ffs(mk) - 1), 1u);  // role (v,w)
+                    }
+                }
+            }
+            hits += seg;
+            if (SUP && seg && !(a.uw & 4)) atomicAdd(a.sup + p, seg);                   // role (u,v)
+        }
+    }
+    add_count(a.count, hits, lane);
+}
+
+// ------------------------------------------------- warp-task kernel (1) --
 template <int TS, bool SUP>
 __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
     uint32_t* const smem = g_dsmem;
@@ -759,11 +817,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[0] > 0) {
         a.tasks = tasks + c->task_off[0];
         a.ntask = c->ntask[0];
-        const size_t smem = kWarps * (SUP ? 3 * kTS0 : kTS0) * sizeof(uint32_t);
         static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_warp<kTS0, SUP>, smem);
-        GC_LAUNCH_S(c, ws, (k_tc_warp<kTS0, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256,
-                    smem, a);
+        if (!grid) grid = occupancy_grid(k_tc_tiny<SUP>, 0);
+        GC_LAUNCH_S(c, ws, (k_tc_tiny<SUP>), (int)std::min<int64_t>(grid, (a.ntask + 255) / 256), 256, 0, a);
     }
     if (fork) {
         GC_CUDA(c, cudaEventRecord(c->ev_join, c->side));
