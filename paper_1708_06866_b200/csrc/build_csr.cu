@@ -17,6 +17,8 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <algorithm>
+
 #include "gc_internal.cuh"
 
 namespace gcx {
@@ -59,15 +61,24 @@ __global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, 
     }
 }
 
-__global__ void k_vkeys(const int32_t* __restrict__ deg, int64_t n, int b, uint64_t* __restrict__ keys) {
-    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
-        keys[x] = ((uint64_t)deg[x] << b) | (uint64_t)x;
+// vertex sort keys: the degree alone, ids as payload (a stable radix sort of
+// ascending ids by degree is the (degree, id) order)
+__global__ void k_vkeys(const int32_t* __restrict__ deg, int64_t n, uint32_t* __restrict__ keys,
+                        int32_t* __restrict__ ids, int* __restrict__ maxdeg) {
+    int mx = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        const int d = deg[x];
+        keys[x] = (uint32_t)d;
+        ids[x] = (int32_t)x;
+        mx = max(mx, d);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) atomicMax(maxdeg, mx);
 }
 
-__global__ void k_rank_scatter(const uint64_t* __restrict__ sorted, int64_t n, uint64_t mask,
-                               int32_t* __restrict__ rank_of) {
+__global__ void k_rank_scatter(const int32_t* __restrict__ sorted_ids, int64_t n, int32_t* __restrict__ rank_of) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-        rank_of[sorted[r] & mask] = (int32_t)r;
+        rank_of[sorted_ids[r]] = (int32_t)r;
 }
 
 // oriented key in rank space: (lo << b) | hi with lo = min rank, hi = max rank
@@ -296,10 +307,25 @@ int build_csr(gc_ctx* c) {
 
     // ---- a4: rank = sorted position of (deg, id); relabel + orient
     if (n > 0) {
-        GC_LAUNCH(c, k_vkeys, grid_for(n), kThreads, 0, c->deg.as<int32_t>(), n, b, c->keys_a.as<uint64_t>());
-        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nullptr, nullptr, n, 2 * b));
-        GC_LAUNCH(c, k_rank_scatter, grid_for(n), kThreads, 0, c->keys_b.as<uint64_t>(), n, mask,
-                  c->rank_of.as<int32_t>());
+        // sort on the degree's bits only (max degree read back first)
+        uint32_t* vk = reinterpret_cast<uint32_t*>(c->keys_a.p);
+        uint32_t* vk_out = vk + n;
+        int32_t* ids = c->vals_a.as<int32_t>();
+        int32_t* ids_out = c->vals_b.as<int32_t>();
+        int* d_maxdeg = d_scal + 4;
+        GC_CUDA(c, cudaMemsetAsync(d_maxdeg, 0, sizeof(int), c->stream));
+        GC_LAUNCH(c, k_vkeys, grid_for(n), kThreads, 0, c->deg.as<int32_t>(), n, vk, ids, d_maxdeg);
+        GC_CUDA(c, cudaMemcpyAsync(h, d_maxdeg, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(sync(c));
+        const int dbits = std::max(1, ceil_log2_u64((uint64_t)reinterpret_cast<int*>(h)[0] + 1));
+        size_t tmp = 0;
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, vk, vk_out, ids, ids_out, n, 0, dbits, c->stream));
+        GC_TRY(ensure(c, c->cub_tmp, tmp));
+        tmp = c->cub_tmp.cap;
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, vk, vk_out, ids, ids_out, n, 0, dbits,
+                                                   c->stream));
+        c->stats.lib_launches += 2 + (dbits + 7) / 8;
+        GC_LAUNCH(c, k_rank_scatter, grid_for(n), kThreads, 0, ids_out, n, c->rank_of.as<int32_t>());
     }
     if (m > 0) {
         GC_LAUNCH(c, k_orient, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->rank_of.as<int32_t>(),

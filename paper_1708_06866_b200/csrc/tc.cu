@@ -132,6 +132,9 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
                             const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col, int force,
                             uint32_t bm_bits, uint32_t* __restrict__ cls, uint64_t* __restrict__ packed,
                             unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int bh[4];                 // per-block class histogram (one global atomic per class)
+    if (threadIdx.x < 4) bh[threadIdx.x] = 0;
+    __syncthreads();
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ntask; j += (int64_t)gridDim.x * blockDim.x) {
         int i0 = sel[j];
         int v = in_dst[i0];
@@ -140,8 +143,11 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
         int k = head_class(dag_ptr, dag_col, in_ptr, v, force, bm_bits);
         cls[j] = (uint32_t)k;
         packed[j] = (uint64_t)(uint32_t)i0 | ((uint64_t)(uint32_t)i1 << 32);
-        atomicAdd(hist + k, 1ULL);
+        const unsigned grp = __match_any_sync(__activemask(), k);    // lanes of one class: one shared atomic
+        if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(bh + k, (unsigned)__popc(grp));
     }
+    __syncthreads();
+    if (threadIdx.x < 4 && bh[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)bh[threadIdx.x]);
 }
 
 // ------------------------------------------------------- stream routine --
