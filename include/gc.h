@@ -151,6 +151,18 @@ int gc_edge_support(gc_ctx* ctx, uint32_t* support_out);
  * k < 2 -> GC_ERR_INVALID; k = 2 -> every edge (vacuous). */
 int gc_ktruss(gc_ctx* ctx, int32_t k, uint8_t* alive_out, int64_t* m_alive);
 
+/* gc_ktruss_analysis: the three results above from ONE support pass — the
+ * north star's own chain ("for each edge (u,v), count |N(u) ∩ N(v)|.
+ * Triangle counting sums this support. k-truss repeats it while peeling").
+ * The support pass finds every triangle once (its hit total is the triangle
+ * count, = Σ support / 3), its per-edge supports are written out, and the
+ * same supports seed the k-truss peel.  Each output pointer may be NULL (not
+ * written); otherwise the same layouts as gc_triangle_count (*triangles),
+ * gc_edge_support (support_out, m uint32) and gc_ktruss (alive_out, m uint8;
+ * *m_alive).  Cold like gc_ktruss.  k < 2 -> GC_ERR_INVALID. */
+int gc_ktruss_analysis(gc_ctx* ctx, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
+                       int64_t* m_alive);
+
 /* gc_truss_decomposition (k = 3 on the full graph, then
  * k + 1 on the result, until empty).  trussness_out[i] = largest k such that
  * canonical edge i is in the k-truss (>= 2); m int32 entries.  *kmax =

@@ -178,7 +178,7 @@ int gc_destroy(gc_ctx* c) {
     gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
                         &c->dag_col, &c->dag_src, &c->dag_eid, &c->in_ptr, &c->in_pos, &c->in_src,
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
-                        &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp,
+                        &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->rem, &c->front_a,
                         &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist};
     for (auto* b : bufs) release(c, *b);
@@ -330,6 +330,15 @@ int gc_ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
     if (!alive_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_ktruss: NULL output");
     cudaSetDevice(c->device);
     return ktruss(c, k, alive_out, m_alive);
+}
+
+int gc_ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
+                       int64_t* m_alive) {
+    GC_TRY(check_ctx(c));
+    if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss_analysis: k must be >= 2 (P:280)");
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss_analysis before gc_build_csr");
+    cudaSetDevice(c->device);
+    return ktruss_analysis(c, k, triangles, support_out, alive_out, m_alive);
 }
 
 int gc_truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {

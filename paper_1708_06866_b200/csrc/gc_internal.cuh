@@ -116,6 +116,7 @@ struct gc_ctx {
     gcx::Buf scal;              // small device scalars (counters, reductions)
     gcx::Buf sup;               // uint32[m] support in DAG-position order
     gcx::Buf out_tmp;           // staging for canonical-order outputs
+    gcx::Buf out_tmp2;          // second staging buffer (fused analysis: support and mask)
 
     // peeler (a8/a9)
     gcx::Buf sym_ptr;   // int64[n+1]
@@ -176,10 +177,13 @@ int build_csr(gc_ctx* c);
 int prepare_tasks(gc_ctx* c);
 int triangle_count(gc_ctx* c, uint64_t* out);
 int support_dag(gc_ctx* c);   // fills c->sup (DAG order), all ranks combined
+unsigned long long* support_hits(gc_ctx* c);   // this rank's triangle count of the last support pass
 int scatter_canonical_u32(gc_ctx* c, const uint32_t* dag_vals, uint32_t* canon_out_dev);
 // peel.cu
 int build_sym(gc_ctx* c);
 int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive);
+int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
+                    int64_t* m_alive);
 int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax);
 // comm.cu
 int nccl_get_unique_id(void* id);

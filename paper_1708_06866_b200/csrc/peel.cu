@@ -658,28 +658,49 @@ static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int6
     return peel_level(c, thr, level, round, removed);
 }
 
-int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
+int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
+                    int64_t* m_alive) {
     const int64_t m = c->m;
+    GC_TRY(host_scratch(c, 4096));
     GC_TRY(record(c, 0));
     GC_TRY(support_dag(c));                 // cold: support computed inside every call
-    GC_TRY(record(c, 2));
-    GC_TRY(peel_setup(c));
-    int64_t removed = 0;
-    if (m > 0 && k > 2) {
-        int32_t round = 0;
-        GC_TRY(peel_any(c, (uint32_t)(k - 2), -1, &round, &removed));
+    if (triangles) {                        // the support pass found every triangle once
+        unsigned long long* hits = support_hits(c);
+        if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(hits), 1));
+        GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 512, hits, 8, cudaMemcpyDeviceToHost, c->stream));
     }
-    GC_TRY(ensure(c, c->out_tmp, (size_t)m));
-    if (m > 0)
-        GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(), m,
-                  c->out_tmp.as<uint8_t>());
+    if (support_out && m > 0) {             // supports before the peel consumes them
+        GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
+        GC_TRY(scatter_canonical_u32(c, c->sup.as<uint32_t>(), c->out_tmp.as<uint32_t>()));
+        GC_TRY(copy_out(c, support_out, c->out_tmp.p, (size_t)m * 4));
+    }
+    GC_TRY(record(c, 2));
+    int64_t removed = 0;
+    if (alive_out || m_alive) {
+        GC_TRY(peel_setup(c));
+        if (m > 0 && k > 2) {
+            int32_t round = 0;
+            GC_TRY(peel_any(c, (uint32_t)(k - 2), -1, &round, &removed));
+        }
+        if (alive_out && m > 0) {
+            GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
+            GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(), m,
+                      c->out_tmp2.as<uint8_t>());
+            GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
+        }
+    }
     GC_TRY(record(c, 1));
-    GC_TRY(copy_out(c, alive_out, c->out_tmp.p, (size_t)m));
     GC_TRY(sync(c));
+    if (triangles) *triangles = *reinterpret_cast<uint64_t*>(static_cast<char*>(c->hpin) + 512);
     if (m_alive) *m_alive = m - removed;
     c->stats.ktruss_ms = elapsed(c, 0, 1);
     c->stats.peel_ms = elapsed(c, 2, 1);
+    c->stats.support_kernel_ms = elapsed(c, 6, 7);
     return GC_OK;
+}
+
+int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
+    return ktruss_analysis(c, k, nullptr, nullptr, alive_out, m_alive);
 }
 
 int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {

@@ -880,6 +880,10 @@ int support_dag(gc_ctx* c) {
     return GC_OK;
 }
 
+unsigned long long* support_hits(gc_ctx* c) {   // triangles found by the last support pass (device)
+    return reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 200);
+}
+
 int scatter_canonical_u32(gc_ctx* c, const uint32_t* dag_vals, uint32_t* out) {
     const int64_t m = c->m;
     if (m == 0) return GC_OK;

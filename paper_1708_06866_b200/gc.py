@@ -46,7 +46,8 @@ GC_OPT_OVERLAP = 13
 EXPORTS = [
     "gc_create", "gc_destroy", "gc_last_error", "gc_nccl_unique_id", "gc_comm_init",
     "gc_comm_init_loopback", "gc_load_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
-    "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_truss_decomposition",
+    "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_ktruss_analysis",
+    "gc_truss_decomposition",
     "gc_set_option", "gc_get_stats", "gc_reset_stats", "gc_partition_bounds",
 ]
 
@@ -101,6 +102,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "gc_triangle_count": ([_vp, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
         "gc_edge_support": ([_vp, _vp], ctypes.c_int),
         "gc_ktruss": ([_vp, _i32, _vp, ctypes.POINTER(_i64)], ctypes.c_int),
+        "gc_ktruss_analysis": ([_vp, _i32, ctypes.POINTER(ctypes.c_uint64), _vp, _vp, ctypes.POINTER(_i64)],
+                               ctypes.c_int),
         "gc_truss_decomposition": ([_vp, _vp, ctypes.POINTER(_i32)], ctypes.c_int),
         "gc_set_option": ([_vp, ctypes.c_int, _i64], ctypes.c_int),
         "gc_get_stats": ([_vp, ctypes.POINTER(gc_stats)], ctypes.c_int),
@@ -246,6 +249,20 @@ class Context:
         ma = _i64()
         self._check(self._L.gc_ktruss(self._h, int(k), _vp(_ptr(out)), ctypes.byref(ma)))
         return out, int(ma.value)
+
+    def ktruss_analysis(self, k: int, support_out=None, mask_out=None):
+        """Triangle count, per-edge support and the k-truss mask from one support pass
+        (gc_ktruss_analysis).  Returns (triangles, support, mask, m_alive)."""
+        m = self.num_edges()
+        if support_out is None:
+            support_out = np.empty(m, dtype=np.uint32)
+        if mask_out is None:
+            mask_out = np.empty(m, dtype=np.uint8)
+        t = ctypes.c_uint64()
+        ma = _i64()
+        self._check(self._L.gc_ktruss_analysis(self._h, int(k), ctypes.byref(t), _vp(_ptr(support_out)),
+                                               _vp(_ptr(mask_out)), ctypes.byref(ma)))
+        return int(t.value), support_out, mask_out, int(ma.value)
 
     def truss_decomposition(self, out=None):
         if out is None:

@@ -473,6 +473,36 @@ def test_partitioned_peeler_c1_and_fixtures(gcmod, parts):
             assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
+# ------------------------------------------------ fused analysis entry point --
+@pytest.mark.parametrize("parts", [0, 3])
+def test_ktruss_analysis_one_pass(gcmod, parts):
+    """gc_ktruss_analysis: triangle count, supports and k-truss mask from one
+    support pass equal the oracle's (and the separate calls'); NULL outputs."""
+    import ctypes
+    cases = [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=41), random_graph(60, 0.4, np.random.default_rng(3))]
+    for u, v in cases:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            if parts:
+                c.comm_init_loopback(parts)
+            c.load_edges(u, v)
+            c.build_csr()
+            for k in (2, 3, 5):
+                T, sup, mask, m_alive = c.ktruss_analysis(k)
+                want, _ = g.ktruss(k)
+                assert T == g.triangle_count() and np.array_equal(sup, g.support())
+                assert np.array_equal(mask, want) and m_alive == int(want.sum())
+            # only the count / only the mask
+            t = ctypes.c_uint64()
+            rc = gcmod.load_library().gc_ktruss_analysis(c._h, 4, ctypes.byref(t), None, None, None)
+            assert rc == 0 and t.value == g.triangle_count()
+            mk = np.empty(g.m, np.uint8)
+            rc = gcmod.load_library().gc_ktruss_analysis(c._h, 4, None, None, mk.ctypes.data, None)
+            assert rc == 0 and np.array_equal(mk, g.ktruss(4)[0])
+            with pytest.raises(gcmod.GcError):
+                c.ktruss_analysis(1)
+
+
 # --------------------------------------------------- API / pointer kinds ----
 def test_device_pointers_and_determinism(ctx):
     import torch
