@@ -124,6 +124,7 @@ struct gc_ctx {
     gcx::Buf sym_eid;   // int32[2m] DAG position of the edge
     bool sym_ready = false;
     bool sym_dirty = true;  // rows were compacted (or never filled): refill before the next peel
+    bool rows_live = false; // rows filled for the current peel call
     gcx::Buf live_len;  // int32[n] live entries at the front of each symmetric row
     gcx::Buf long_rows; // int32 rows longer than kLongRow (compacted block-wide)
     int nlong = 0;

@@ -450,6 +450,7 @@ static int sym_refill(gc_ctx* c) {
 // Drop dead entries from the rows once the live edge count has fallen to
 // 1/compact_div of what it was at the last compaction (or the start).
 static int maybe_compact(gc_ctx* c) {
+    if (!c->rows_live) return GC_OK;
     if (c->compact_div <= 1 || c->m_alive_h <= 0 || c->m_alive_h * c->compact_div > c->compact_at) return GC_OK;
     const int64_t n = c->n, m = c->m;
     GC_TRY(record(c, 12));
@@ -469,6 +470,17 @@ static int maybe_compact(gc_ctx* c) {
     c->compact_at = c->m_alive_h;
     c->sym_dirty = true;              // the next peel call refills the rows
     c->stats.compactions++;
+    return GC_OK;
+}
+
+// Symmetric rows are needed only once a round has triangles to destroy (the
+// k = 3 peel removes its zero-support edges during the scan and never needs
+// them): built / refilled on first use within a peel call.
+static int ensure_rows(gc_ctx* c) {
+    if (c->rows_live) return GC_OK;
+    GC_TRY(build_sym(c));
+    if (c->sym_dirty) GC_TRY(sym_refill(c));
+    c->rows_live = true;
     return GC_OK;
 }
 
@@ -511,6 +523,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         c->m_alive_h -= z;
     }
     int nf = h[0];
+    if (nf > 0) GC_TRY(ensure_rows(c));
     // Rounds are enqueued in batches without a host round trip: each round's
     // kernels read the frontier size on the device (an empty frontier makes a
     // round a no-op), and the host looks at the next frontier size only after
@@ -600,6 +613,7 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         GC_TRY(sync(c));
         const int nf = h[0];
         if (nf == 0) break;
+        GC_TRY(ensure_rows(c));
         GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
         for (int r = r_begin; r < r_end; ++r) {
             PolicyPart pol{xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb};
@@ -618,7 +632,7 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
 
 static int peel_setup(gc_ctx* c) {
     const int64_t m = c->m;
-    GC_TRY(build_sym(c));
+    c->rows_live = false;
     GC_TRY(ensure(c, c->alive, (size_t)m));
     GC_TRY(ensure(c, c->rem, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_a, (size_t)m * 4));
@@ -626,7 +640,6 @@ static int peel_setup(gc_ctx* c) {
     GC_TRY(ensure(c, c->alist, (size_t)m * 4));
     GC_TRY(ensure(c, c->scal, 1024));
     GC_TRY(host_scratch(c, 4096));
-    if (c->sym_dirty) GC_TRY(sym_refill(c));
     c->m_alive_h = m;
     c->compact_at = m;
     c->alist_n = -1;
