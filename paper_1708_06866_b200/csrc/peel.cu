@@ -395,6 +395,13 @@ __global__ void k_finish_round_dev(const int32_t* __restrict__ front, const int*
     }
 }
 
+// mask from the canonical supports when the peel ran no round: it then only
+// removed zero-support edges (at the level scan), so alive = (S >= 1)
+__global__ void k_mask_from_support(const uint32_t* __restrict__ sup_canon, int64_t m, uint8_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = sup_canon[i] != 0u;
+}
+
 __global__ void k_scatter_u8(const uint8_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
                              uint8_t* __restrict__ out) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
@@ -697,8 +704,15 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
         }
         if (alive_out && m > 0) {
             GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
-            GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(), m,
-                      c->out_tmp2.as<uint8_t>());
+            if (support_out && c->stats.peel_rounds == 0 && k > 2) {
+                // no round ran: only zero-support edges left, read the mask off the
+                // canonical supports (coalesced) instead of scattering the DAG-order one
+                GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->out_tmp.as<uint32_t>(), m,
+                          c->out_tmp2.as<uint8_t>());
+            } else {
+                GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(),
+                          m, c->out_tmp2.as<uint8_t>());
+            }
             GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
         }
     }
