@@ -12,7 +12,7 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            --expt-relaxed-constexpr -Iinclude
 PKG     := paper_1708_06866_b200
 CSRC    := $(PKG)/csrc
-GC_SRCS := $(CSRC)/gc_api.cu $(CSRC)/build_csr.cu $(CSRC)/tc.cu $(CSRC)/peel.cu $(CSRC)/comm.cu
+GC_SRCS := $(CSRC)/gc_api.cu $(CSRC)/build_csr.cu $(CSRC)/tc.cu $(CSRC)/peel.cu $(CSRC)/listing.cu $(CSRC)/comm.cu
 GC_HDRS := $(CSRC)/gc_internal.cuh include/gc.h
 GC_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(GC_SRCS))
 

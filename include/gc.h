@@ -163,6 +163,15 @@ int gc_ktruss(gc_ctx* ctx, int32_t k, uint8_t* alive_out, int64_t* m_alive);
 int gc_ktruss_analysis(gc_ctx* ctx, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
                        int64_t* m_alive);
 
+/* gc_list_triangles (Alg. 1's triangle records; SURVEY §8(f)
+ * NEXT #3): every triangle once as three ORIGINAL vertex ids, ascending
+ * within the triple; triples in unspecified order.  tri_out: 3 * capacity
+ * int32 (host or device); *count = the number of triangles T.  capacity < T
+ * -> GC_ERR_RANGE with *count set and nothing written (call again with a
+ * buffer of 3 * T).  Includes a triangle-count pass; runs on this rank alone
+ * (every rank of a communicator lists the whole graph). */
+int gc_list_triangles(gc_ctx* ctx, int32_t* tri_out, int64_t capacity, int64_t* count);
+
 /* gc_truss_decomposition (k = 3 on the full graph, then
  * k + 1 on the result, until empty).  trussness_out[i] = largest k such that
  * canonical edge i is in the k-truss (>= 2); m int32 entries.  *kmax =

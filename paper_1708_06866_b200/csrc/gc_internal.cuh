@@ -117,6 +117,8 @@ struct gc_ctx {
     gcx::Buf sup;               // uint32[m] support in DAG-position order
     gcx::Buf out_tmp;           // staging for canonical-order outputs
     gcx::Buf out_tmp2;          // second staging buffer (fused analysis: support and mask)
+    gcx::Buf id_of;             // int32[n] rank -> original id (triangle listing)
+    gcx::Buf list_out;          // int32[3T] listed triangles
 
     // peeler (a8/a9)
     gcx::Buf sym_ptr;   // int64[n+1]
@@ -186,6 +188,8 @@ int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive);
 int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
                     int64_t* m_alive);
 int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax);
+// listing.cu
+int list_triangles(gc_ctx* c, int32_t* tri_out, int64_t capacity, int64_t* count);
 // comm.cu
 int nccl_get_unique_id(void* id);
 int nccl_init(gc_ctx* c, const void* id, int nranks, int rank);

@@ -47,7 +47,7 @@ EXPORTS = [
     "gc_create", "gc_destroy", "gc_last_error", "gc_nccl_unique_id", "gc_comm_init",
     "gc_comm_init_loopback", "gc_load_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
     "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_ktruss_analysis",
-    "gc_truss_decomposition",
+    "gc_truss_decomposition", "gc_list_triangles",
     "gc_set_option", "gc_get_stats", "gc_reset_stats", "gc_partition_bounds",
 ]
 
@@ -105,6 +105,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "gc_ktruss_analysis": ([_vp, _i32, ctypes.POINTER(ctypes.c_uint64), _vp, _vp, ctypes.POINTER(_i64)],
                                ctypes.c_int),
         "gc_truss_decomposition": ([_vp, _vp, ctypes.POINTER(_i32)], ctypes.c_int),
+        "gc_list_triangles": ([_vp, _vp, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
         "gc_set_option": ([_vp, ctypes.c_int, _i64], ctypes.c_int),
         "gc_get_stats": ([_vp, ctypes.POINTER(gc_stats)], ctypes.c_int),
         "gc_reset_stats": ([_vp], ctypes.c_int),
@@ -270,6 +271,16 @@ class Context:
         km = _i32()
         self._check(self._L.gc_truss_decomposition(self._h, _vp(_ptr(out)), ctypes.byref(km)))
         return out, int(km.value)
+
+    def list_triangles(self, capacity: int | None = None):
+        """All triangles as an int32 array [T, 3] of original ids (ascending within
+        a row; rows in unspecified order) -- gc_list_triangles."""
+        cnt = _i64()
+        if capacity is None:
+            capacity = self.triangle_count()
+        out = np.empty((max(int(capacity), 1), 3), dtype=np.int32)
+        self._check(self._L.gc_list_triangles(self._h, _vp(_ptr(out)), int(capacity), ctypes.byref(cnt)))
+        return out[:cnt.value]
 
     def set_option(self, option: int, value: int):
         self._check(self._L.gc_set_option(self._h, int(option), int(value)))

@@ -473,6 +473,45 @@ def test_partitioned_peeler_c1_and_fixtures(gcmod, parts):
             assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
+# ------------------------------------------------------- triangle listing ----
+def _brute_triangles(g):
+    """Independent listing from the oracle's canonical edges: {a<b<w} with all three edges present."""
+    adj = {}
+    for a, b in zip(g.cu.tolist(), g.cv.tolist()):
+        adj.setdefault(a, set()).add(b)
+        adj.setdefault(b, set()).add(a)
+    out = set()
+    for a, b in zip(g.cu.tolist(), g.cv.tolist()):
+        for w in adj[a] & adj[b]:
+            if w > b:
+                out.add((a, b, w))
+    return out
+
+
+def test_list_triangles(gcmod, ctx):
+    """gc_list_triangles (Alg. 1's triangle records): the same set as
+    an independent enumeration, each triangle once, ids ascending in a row;
+    the king grid's triangles all sit inside 2x2 pixel cells."""
+    for u, v in [gen.CONFIGS["C1"].generate(), gen.rmat(11, 16, seed=43), random_graph(70, 0.3, np.random.default_rng(9))]:
+        g = oracle.OracleGraph(u, v)
+        run_gpu(ctx, u, v)
+        tri = ctx.list_triangles()
+        assert tri.shape == (g.triangle_count(), 3)
+        assert np.all(tri[:, 0] < tri[:, 1]) and np.all(tri[:, 1] < tri[:, 2])
+        got = set(map(tuple, tri.tolist()))
+        assert len(got) == len(tri) and got == _brute_triangles(g)
+    M = 64
+    u, v = gen.king_grid(M)
+    run_gpu(ctx, u, v)
+    tri = ctx.list_triangles()
+    assert len(tri) == 4 * (M - 1) ** 2
+    r, c = tri // M, tri % M
+    assert np.all(r.max(1) - r.min(1) == 1) and np.all(c.max(1) - c.min(1) == 1)
+    with pytest.raises(gcmod.GcError) as e:
+        ctx.list_triangles(capacity=10)
+    assert e.value.code == gcmod.GC_ERR_RANGE
+
+
 # ------------------------------------------------ fused analysis entry point --
 @pytest.mark.parametrize("parts", [0, 3])
 def test_ktruss_analysis_one_pass(gcmod, parts):
