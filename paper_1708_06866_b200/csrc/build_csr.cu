@@ -52,13 +52,25 @@ __global__ void k_pack(const int32_t* __restrict__ u, const int32_t* __restrict_
     }
 }
 
-__global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ deg) {
+// Degrees from the canonical list (sorted by (lo, hi)): the lo side is the
+// length of each lo run (its bounds written, no atomics), the hi side one
+// atomic per edge.
+__global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ deg,
+                          int32_t* __restrict__ first, int32_t* __restrict__ last) {
     const uint64_t mask = (1ULL << b) - 1;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t k = canon[e];
-        atomicAdd(deg + (k >> b), 1);
+        const uint64_t k = canon[e];
+        const uint32_t lo = (uint32_t)(k >> b);
         atomicAdd(deg + (k & mask), 1);
+        if (e == 0 || (uint32_t)(canon[e - 1] >> b) != lo) first[lo] = (int32_t)e;
+        if (e == m - 1 || (uint32_t)(canon[e + 1] >> b) != lo) last[lo] = (int32_t)(e + 1);
     }
+}
+
+__global__ void k_degrees_lo(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int64_t n,
+                             int32_t* __restrict__ deg) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        deg[x] += last[x] - first[x];
 }
 
 // vertex sort keys: the degree alone, ids as payload (a stable radix sort of
@@ -122,15 +134,21 @@ __global__ void k_row_len(const int32_t* __restrict__ first, const int32_t* __re
         len[x] = (x < n) ? (int64_t)(last[x] - first[x]) : 0;
 }
 
-__global__ void k_iota(int32_t* __restrict__ a, int64_t m) {
+
+// in-list sort payload: (tail << 32) | DAG position, so the sort carries the
+// tail along (no gather afterwards)
+__global__ void k_pos_tail(const int32_t* __restrict__ dag_src, int64_t m, uint64_t* __restrict__ vals) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
-        a[p] = (int32_t)p;
+        vals[p] = ((uint64_t)(uint32_t)dag_src[p] << 32) | (uint64_t)(uint32_t)p;
 }
 
-__global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t m,
-                             int32_t* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = src[idx[i]];
+__global__ void k_split_pos_tail(const uint64_t* __restrict__ vals, int64_t m, int32_t* __restrict__ pos,
+                                 int32_t* __restrict__ tail) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = vals[i];
+        pos[i] = (int32_t)(uint32_t)x;
+        tail[i] = (int32_t)(x >> 32);
+    }
 }
 
 // Work-model sums over vertices: wedges = Σ C(d+,2), Q_out = Σ d+², Q_in = Σ d- d+,
@@ -302,8 +320,15 @@ int build_csr(gc_ctx* c) {
     GC_TRY(ensure(c, c->keys_a, (size_t)(m > n ? m : n) * 8));
     GC_TRY(ensure(c, c->keys_b, (size_t)(m > n ? m : n) * 8));
     GC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)n * 4, c->stream));
-    if (m > 0)
-        GC_LAUNCH(c, k_degrees, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->deg.as<int32_t>());
+    if (m > 0) {
+        int32_t* first = c->vals_a.as<int32_t>();        // n entries each; zero = no lo run
+        int32_t* last = c->vals_b.as<int32_t>();
+        GC_CUDA(c, cudaMemsetAsync(first, 0, (size_t)n * 4, c->stream));
+        GC_CUDA(c, cudaMemsetAsync(last, 0, (size_t)n * 4, c->stream));
+        GC_LAUNCH(c, k_degrees, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->deg.as<int32_t>(),
+                  first, last);
+        GC_LAUNCH(c, k_degrees_lo, grid_for(n), kThreads, 0, first, last, n, c->deg.as<int32_t>());
+    }
 
     // ---- a4: rank = sorted position of (deg, id); relabel + orient
     if (n > 0) {
@@ -340,18 +365,18 @@ int build_csr(gc_ctx* c) {
     if (m > 0) {
         // DAG order is sorted by (tail, head): a stable sort on the head alone
         // (b-bit keys, 32-bit) groups in-edges by head with tails ascending.
-        GC_LAUNCH(c, k_iota, grid_for(m), kThreads, 0, c->vals_a.as<int32_t>(), m);
+        uint64_t* pv = c->keys_a.as<uint64_t>();          // free after the orientation sort
+        uint64_t* pv_out = c->keys_b.as<uint64_t>();
+        GC_LAUNCH(c, k_pos_tail, grid_for(m), kThreads, 0, c->dag_src.as<int32_t>(), m, pv);
         size_t tmp = 0;
         const uint32_t* hk = reinterpret_cast<const uint32_t*>(c->dag_col.p);
         uint32_t* hk_out = reinterpret_cast<uint32_t*>(c->in_dst.p);
-        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, hk, hk_out, c->vals_a.as<int32_t>(),
-                                                   c->in_pos.as<int32_t>(), m, 0, b, c->stream));
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, hk, hk_out, pv, pv_out, m, 0, b, c->stream));
         GC_TRY(ensure(c, c->cub_tmp, tmp));
         tmp = c->cub_tmp.cap;
-        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hk, hk_out, c->vals_a.as<int32_t>(),
-                                                   c->in_pos.as<int32_t>(), m, 0, b, c->stream));
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hk, hk_out, pv, pv_out, m, 0, b, c->stream));
         c->stats.lib_launches += 2 + (b + 7) / 8;
-        GC_LAUNCH(c, k_gather_i32, grid_for(m), kThreads, 0, c->dag_src.as<int32_t>(), c->in_pos.as<int32_t>(), m,
+        GC_LAUNCH(c, k_split_pos_tail, grid_for(m), kThreads, 0, pv_out, m, c->in_pos.as<int32_t>(),
                   c->in_src.as<int32_t>());
     }
     GC_TRY(csr_ptr_from_sorted(c, c->in_dst.as<int32_t>(), m, n, c->in_ptr.as<int64_t>()));
