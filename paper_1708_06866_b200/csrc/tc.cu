@@ -58,6 +58,18 @@ constexpr int kTS2 = 4096;     // heavy-head hash slots when the bitmap does not
 constexpr int kTS3 = 16384;    // huge-head hash slots (d+ <= kTS3/2 by default)
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
+#ifndef GC_SUP_WARPS
+#define GC_SUP_WARPS 10                     // heavy-head support kernel: warps per block sharing one table
+#endif
+#ifndef GC_SUP_MINB
+#define GC_SUP_MINB 4                       // ... and resident blocks per SM (register budget)
+#endif
+#ifndef GC_TC_WARPS
+#define GC_TC_WARPS 8                       // heavy-head count kernel: warps per block
+#endif
+#ifndef GC_TC_MINB
+#define GC_TC_MINB 6
+#endif
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
 // tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
@@ -516,7 +528,10 @@ struct GlobalProbe {
 };
 
 template <bool SUP, bool HUGE>
-__global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArgs a) {
+__global__ void __launch_bounds__(HUGE ? 256 : 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS),
+                                  HUGE ? 1 : (SUP ? GC_SUP_MINB : GC_TC_MINB))
+    k_tc_block(KArgs a) {
+    constexpr int BW = HUGE ? kWarps : SUP ? GC_SUP_WARPS : GC_TC_WARPS;   // warps per block (= blockDim.x / 32)
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
@@ -616,7 +631,7 @@ __global__ void __launch_bounds__(256, HUGE ? 1 : (SUP ? 4 : 6)) k_tc_block(KArg
         }
         // this warp's eighth of the task's cost units
         const int64_t c0 = __ldg(a.in_cost + i0), c1 = __ldg(a.in_cost + i1);
-        const int64_t ca = c0 + (c1 - c0) * warp / kWarps, cb = c0 + (c1 - c0) * (warp + 1) / kWarps;
+        const int64_t ca = c0 + (c1 - c0) * warp / BW, cb = c0 + (c1 - c0) * (warp + 1) / BW;
         if (cb > ca) {
             const int first = (int)warp_lower_bound(a.in_cost, i0, i1, ca + 1, lane) - 1;
             const int end = (int)warp_lower_bound(a.in_cost, i0, i1, cb, lane);
@@ -647,9 +662,9 @@ __global__ void k_scatter_u32(const uint32_t* __restrict__ vals, const int32_t* 
 }
 
 template <class K>
-int occupancy_grid(K kernel, size_t smem) {
+int occupancy_grid(K kernel, size_t smem, int threads = 256) {
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, 256, smem) != cudaSuccess || blocks < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, threads, smem) != cudaSuccess || blocks < 1) {
         cudaGetLastError();
         blocks = 1;
     }
@@ -801,9 +816,10 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
                                             (int)smem));
             attr_set[SUP] = true;
         }
+        constexpr int threads = 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS);
         static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_block<SUP, false>, smem);
-        GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
+        if (!grid) grid = occupancy_grid(k_tc_block<SUP, false>, smem, threads);
+        GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
     }
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
