@@ -64,6 +64,13 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #ifndef GC_SUP_MINB
 #define GC_SUP_MINB 4                       // ... and resident blocks per SM (register budget)
 #endif
+#ifndef GC_HUGE_WARPS_TC
+#define GC_HUGE_WARPS_TC 16                 // huge-head kernels (class 3): warps per block sharing the
+#endif                                      // table (1-3 resident blocks per SM: more warps hide latency)
+#ifndef GC_HUGE_WARPS_SUP
+#define GC_HUGE_WARPS_SUP 32
+#endif
+#define GC_HUGE_WARPS(S) ((S) ? GC_HUGE_WARPS_SUP : GC_HUGE_WARPS_TC)
 #ifndef GC_TC_WARPS
 #define GC_TC_WARPS 8                       // heavy-head count kernel: warps per block
 #endif
@@ -528,10 +535,10 @@ struct GlobalProbe {
 };
 
 template <bool SUP, bool HUGE>
-__global__ void __launch_bounds__(HUGE ? 256 : 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS),
+__global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS),
                                   HUGE ? 1 : (SUP ? GC_SUP_MINB : GC_TC_MINB))
     k_tc_block(KArgs a) {
-    constexpr int BW = HUGE ? kWarps : SUP ? GC_SUP_WARPS : GC_TC_WARPS;   // warps per block (= blockDim.x / 32)
+    constexpr int BW = HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS;   // warps per block (= blockDim.x / 32)
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
@@ -802,9 +809,10 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
                                             (int)smem));
             attr_set[SUP] = true;
         }
+        constexpr int threads = 32 * GC_HUGE_WARPS(SUP);
         static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_block<SUP, true>, smem);
-        GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), 256, smem, a);
+        if (!grid) grid = occupancy_grid(k_tc_block<SUP, true>, smem, threads);
+        GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
     }
     if (c->ntask[2] > 0) {
         a.tasks = tasks + c->task_off[2];
