@@ -44,7 +44,7 @@ constexpr int kOvh = 2;                     // per in-edge overhead in the cost 
 #define GC_KD1 128
 #endif
 constexpr int kD0 = 8, kD1 = GC_KD1, kD2 = 4096;    // class bounds on d+(v)
-constexpr int kTS1 = 512;
+constexpr int kTS1 = 2 * kD1;   // class-1 warp hash slots: load <= 1/2 at d+ = kD1
 constexpr int64_t kTinyChunk = 256;   // class-0 task budget: one task per lane, keep lanes even
 #ifndef GC_TINY_IN
 #define GC_TINY_IN 64
