@@ -10,8 +10,11 @@ names = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.su
          "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread", "launch__grid_size"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 rows = {}
-for rep in ["prof_tc_c4", "prof_tc_warp_c4", "prof_sup_block_c4", "prof_sup_warp_c4"]:
+for rep in ["prof_tc_c4", "prof_tc_warp_c4", "prof_tc_tiny_c4", "prof_sup_block_c4", "prof_sup_warp_c4",
+            "prof_sup_tiny_c4"]:
     path = os.path.join(g, rep + ".ncu-rep")
+    if not os.path.exists(path):
+        continue
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     h, u = r[0], r[1]
@@ -25,9 +28,9 @@ for rep in ["prof_tc_c4", "prof_tc_warp_c4", "prof_sup_block_c4", "prof_sup_warp
 def dram(k):
     d = rows[k]
     return sum(float(d[n][0]) * scale.get(d[n][1], 1) for n in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-def is_sup(k):   # k_tc_block<SUP, HUGE>, k_tc_warp<TS, SUP>
+def is_sup(k):   # k_tc_block<SUP, HUGE>, k_tc_warp<TS, SUP>, k_tc_tiny<SUP>
     args = [a.strip() for a in k[k.index("<") + 1:k.rindex(">")].split(",")]
-    return (args[0] if k.startswith("k_tc_block") else args[1]) == "1"
+    return (args[1] if k.startswith("k_tc_warp") else args[0]) == "1"
 passes = {"tc": [k for k in rows if not is_sup(k)], "support": [k for k in rows if is_sup(k)]}
 summ = {"workload": "C4 R-MAT s24", "source": f"profiles/{tag}/ncu_passes.md"}
 for p, ks in passes.items():

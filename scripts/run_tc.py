@@ -24,6 +24,9 @@ for r in range(a.reps):
         T = ctx.triangle_count()
     if "support" in a.what:
         ctx.edge_support(torch.empty(ctx.num_edges(), dtype=torch.int32, device="cuda"))
+    if "analysis" in a.what:
+        ctx.ktruss_analysis(3, torch.empty(ctx.num_edges(), dtype=torch.int32, device="cuda"),
+                            torch.empty(ctx.num_edges(), dtype=torch.uint8, device="cuda"))
     if "ktruss" in a.what:
         ctx.ktruss(3, torch.empty(ctx.num_edges(), dtype=torch.uint8, device="cuda"))
     st = ctx.stats()
