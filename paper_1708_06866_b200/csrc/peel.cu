@@ -278,47 +278,93 @@ struct PeelArgs {
     const uint8_t* alive;
 };
 
-// One warp per frontier edge e = (a, b): destroy its live triangles by
-// walking the shorter endpoint row (lanes over its entries) and binary-
-// searching each live entry in the longer one (rows sorted by rank; dead
-// entries compacted away now and then).  Stop once S(e) live triangles are
-// found (S exact only for the single-rank policy).  Measured alternatives
-// (DESIGN.md): one lane per short-row edge, 32-ary window narrowing, and
-// splitting long rows into work items over many warps were all slower at C4
-// and C5, where the big early rounds dominate.
+// Destroy the live triangles of each frontier edge e = (a, b): walk the
+// shorter endpoint row and binary-search each live entry in the longer one
+// (rows sorted by rank; dead entries compacted away now and then).  Stop
+// once S(e) live triangles are found (S exact only for the single-rank
+// policy).  A warp takes G frontier edges at a time (G = 1 for small
+// frontiers, up to 32 for big ones): lanes whose shorter row has at most
+// kSerialRow entries walk it alone (uniform-degree graphs: every lane busy),
+// the other edges are walked by the whole warp one after another.  Measured
+// alternatives: 32-ary window narrowing of the longer row and
+// splitting long rows into work items over many warps were slower.
+constexpr int kSerialRow = 8;
+#ifndef GC_PEEL_GMAX
+#define GC_PEEL_GMAX 8   // frontier edges per warp at most (8: K13 kernel 226 -> 78 ms, C4 +0.7 %)
+#endif
+
+template <class Pol>
+__device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol, int e, uint32_t live, int64_t a0,
+                                              int64_t a1, int64_t b0, int64_t b1, int lane) {
+    uint32_t found = 0;
+    for (int64_t base = a0; base < a1 && found < live; base += 32) {
+        const int64_t i = base + lane;
+        bool tri = false;
+        int f = -1, g = -1;
+        if (i < a1) {
+            f = __ldg(A.sym_eid + i);
+            if (f != e && A.alive[f]) {
+                const int32_t w = __ldg(A.sym_col + i);
+                const int64_t j = lower_bound_i32(A.sym_col, b0, b1, w);
+                if (j < b1 && __ldg(A.sym_col + j) == w) {
+                    g = __ldg(A.sym_eid + j);
+                    tri = A.alive[g] != 0;
+                }
+            }
+        }
+        found += __popc(__ballot_sync(0xffffffffu, tri));
+        if (tri) destroy(pol, e, f, g);
+    }
+}
+
 template <class Pol>
 __global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int nfront = A.nfront_dev ? *A.nfront_dev : A.nfront;
-    for (int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nfront; wi += warps) {
-        const int e = A.front[wi];
-        const uint32_t live = pol.live(e);
-        if (live == 0) continue;                 // no live triangle (the whole k = 3 peel)
-        const int a = A.dag_src[e], b = A.dag_col[e];
-        int64_t a0 = A.sym_ptr[a], a1 = a0 + A.live_len[a], b0 = A.sym_ptr[b], b1 = b0 + A.live_len[b];
-        if (a1 - a0 > b1 - b0) {
-            int64_t t0 = a0, t1 = a1;
-            a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+    const int G = (int)max((int64_t)1, min((int64_t)GC_PEEL_GMAX, nfront / warps));     // edges per warp
+    for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G; base < nfront;
+         base += warps * G) {
+        int e = -1;
+        uint32_t live = 0;
+        int64_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        if (lane < G && base + lane < nfront) {
+            e = A.front[base + lane];
+            live = pol.live(e);
+            if (live) {
+                const int a = A.dag_src[e], b = A.dag_col[e];
+                a0 = A.sym_ptr[a]; a1 = a0 + A.live_len[a]; b0 = A.sym_ptr[b]; b1 = b0 + A.live_len[b];
+                if (a1 - a0 > b1 - b0) {
+                    int64_t t0 = a0, t1 = a1;
+                    a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+                }
+            }
         }
-        uint32_t found = 0;
-        for (int64_t base = a0; base < a1 && found < live; base += 32) {
-            const int64_t i = base + lane;
-            bool tri = false;
-            int f = -1, g = -1;
-            if (i < a1) {
-                f = __ldg(A.sym_eid + i);
-                if (f != e && A.alive[f]) {
-                    const int32_t w = __ldg(A.sym_col + i);
-                    const int64_t j = lower_bound_i32(A.sym_col, b0, b1, w);
-                    if (j < b1 && __ldg(A.sym_col + j) == w) {
-                        g = __ldg(A.sym_eid + j);
-                        tri = A.alive[g] != 0;
+        const bool serial = live && G > 1 && a1 - a0 <= kSerialRow;
+        if (serial) {                                   // this lane alone
+            uint32_t found = 0;
+            int64_t lo = b0;
+            for (int64_t i = a0; i < a1 && found < live; ++i) {
+                const int f = __ldg(A.sym_eid + i);
+                if (f == e || !A.alive[f]) continue;
+                const int32_t w = __ldg(A.sym_col + i);
+                lo = lower_bound_i32(A.sym_col, lo, b1, w);   // targets ascend along the row
+                if (lo < b1 && __ldg(A.sym_col + lo) == w) {
+                    const int g = __ldg(A.sym_eid + lo);
+                    if (A.alive[g]) {
+                        ++found;
+                        destroy(pol, e, f, g);
                     }
                 }
             }
-            found += __popc(__ballot_sync(0xffffffffu, tri));
-            if (tri) destroy(pol, e, f, g);
+        }
+        unsigned coop = __ballot_sync(0xffffffffu, live && !serial);
+        while (coop) {                                  // the whole warp, one edge at a time
+            const int src = __ffs(coop) - 1;
+            coop &= coop - 1;
+            peel_one_warp(A, pol, __shfl_sync(0xffffffffu, e, src), __shfl_sync(0xffffffffu, live, src),
+                          __shfl_sync(0xffffffffu, a0, src), __shfl_sync(0xffffffffu, a1, src),
+                          __shfl_sync(0xffffffffu, b0, src), __shfl_sync(0xffffffffu, b1, src), lane);
         }
     }
 }

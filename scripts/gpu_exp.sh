@@ -1,3 +1,1 @@
-timeout 600 python scripts/tune.py C4 "overlap=1" 2>&1 | tail -1
-timeout 600 python scripts/tune.py C3 "overlap=1" 2>&1 | tail -1
-timeout 900 python -m pytest tests -m gpu -x -q -p no:warnings -k "huge or forced or clique or c3 or c1 or c2" 2>&1 | tail -1
+for G in 4 8 16; do echo G=$G; for C in C4 K13; do GC_LIB_PATH=exp/libgc_g$G.so timeout 900 python scripts/run_decomp.py --config $C 2>&1 | tail -1; done; done
