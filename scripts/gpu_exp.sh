@@ -1,1 +1,1 @@
-for G in 4 8 16; do echo G=$G; for C in C4 K13; do GC_LIB_PATH=exp/libgc_g$G.so timeout 900 python scripts/run_decomp.py --config $C 2>&1 | tail -1; done; done
+for L in s12_4 s16_3 s10_4; do echo $L; GC_LIB_PATH=exp/libgc_$L.so timeout 600 python scripts/tune.py C4 "overlap=1" 2>&1 | tail -1; done
