@@ -21,6 +21,10 @@
 
 #include "gc_internal.cuh"
 
+#ifndef GC_SPLIT_SORT1
+#define GC_SPLIT_SORT1 1   // canonicalisation sort as two 32-bit pair sorts (hi, then lo)
+#endif
+
 namespace gcx {
 
 namespace {
@@ -55,6 +59,24 @@ __global__ void k_pack(const int32_t* __restrict__ u, const int32_t* __restrict_
 // Degrees from the canonical list (sorted by (lo, hi)): the lo side is the
 // length of each lo run (its bounds written, no atomics), the hi side one
 // atomic per edge.
+// split keys for the canonicalisation sort: lo = min, hi = max as two 32-bit
+// arrays; a self loop becomes (2^b - 1, 2^b - 1), which sorts last and is no
+// real edge (lo < hi for every real one)
+__global__ void k_pack_split(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz, uint32_t sent,
+                             uint32_t* __restrict__ lo_out, uint32_t* __restrict__ hi_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
+        lo_out[i] = a == c ? sent : min(a, c);
+        hi_out[i] = a == c ? sent : max(a, c);
+    }
+}
+
+__global__ void k_join_keys(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, int64_t nnz, int b,
+                            uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = ((uint64_t)lo[i] << b) | hi[i];
+}
+
 __global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ deg,
                           int32_t* __restrict__ first, int32_t* __restrict__ last) {
     const uint64_t mask = (1ULL << b) - 1;
@@ -279,9 +301,29 @@ int build_csr(gc_ctx* c) {
         GC_TRY(ensure(c, c->keys_a, (size_t)nnz * 8));
         GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
         const uint64_t sent = (2 * b >= 64) ? ~0ULL : ((1ULL << (2 * b)) - 1);
-        GC_LAUNCH(c, k_pack, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz, b, sent,
-                  c->keys_a.as<uint64_t>());
-        GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nullptr, nullptr, nnz, 2 * b));
+        if (GC_SPLIT_SORT1 && b <= 31) {
+            // (lo, hi) order by two stable 32-bit pair sorts, hi then lo: the same
+            // bytes per pass as one 64-bit key sort, with 32-bit digits passes
+            uint32_t* lo_a = reinterpret_cast<uint32_t*>(c->keys_a.p);
+            uint32_t* hi_a = lo_a + nnz;
+            uint32_t* lo_b = reinterpret_cast<uint32_t*>(c->keys_b.p);
+            uint32_t* hi_b = lo_b + nnz;
+            GC_LAUNCH(c, k_pack_split, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
+                      (uint32_t)((1ULL << b) - 1), lo_a, hi_a);
+            size_t tmp = 0;
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, hi_a, hi_b, lo_a, lo_b, nnz, 0, b, c->stream));
+            GC_TRY(ensure(c, c->cub_tmp, tmp));
+            tmp = c->cub_tmp.cap;
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hi_a, hi_b, lo_a, lo_b, nnz, 0, b, c->stream));
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, lo_b, lo_a, hi_b, hi_a, nnz, 0, b, c->stream));
+            c->stats.lib_launches += 2 * (2 + (b + 7) / 8);
+            // joined 64-bit keys into keys_b (lo_b/hi_b are consumed)
+            GC_LAUNCH(c, k_join_keys, grid_for(nnz), kThreads, 0, lo_a, hi_a, nnz, b, c->keys_b.as<uint64_t>());
+        } else {
+            GC_LAUNCH(c, k_pack, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz, b,
+                      sent, c->keys_a.as<uint64_t>());
+            GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nullptr, nullptr, nnz, 2 * b));
+        }
         GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
         int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
         size_t tmp = 0;
