@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--ktruss-k", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extra", action="store_true", help="skip the k = 4..6 trusses and the decomposition")
     p.add_argument("--cpu-sample", type=int, default=1 << 20, help="edges in the oracle's support sample")
     return p.parse_args()
 
@@ -322,6 +323,19 @@ def main():
     sep_ms = timed(separate_step, args.steps)
     tck = float(np.mean(sep["tc_kernel_ms"]))
 
+    # ---- deeper trusses and the decomposition on the same graph (reported, not the step)
+    deeper = {}
+    if not args.no_extra:
+        for kk in (4, 5, 6):
+            t = timed(lambda: ctx.ktruss_analysis(kk, sup_out, mask_out), 1)
+            deeper[f"ktruss_analysis_k{kk}_ms"] = t
+            deeper[f"k{kk}_peel_rounds"] = ctx.stats()["peel_rounds"]
+        tau_out = torch.empty(m, dtype=torch.int32, device="cuda")
+        res = {}
+        t = timed(lambda: res.update(kmax=ctx.truss_decomposition(tau_out)[1]), 1)
+        deeper.update({"decomposition_ms": t, "kmax": res.get("kmax"),
+                       "decomposition_rounds": ctx.stats()["peel_rounds"]})
+
     # ---- roofline of the dominant kernel: the support intersection pass; TC pass beside it
     peak, peak_src = hbm_peak()
     b_tc = algorithmic_bytes_tc(st)
@@ -408,6 +422,7 @@ def main():
                                "step": f"gc_build_csr + gc_triangle_count + gc_edge_support + gc_ktruss(k={k}) "
                                        "(each call cold: two support passes and a TC pass)"},
             "tc_rate_edges_per_s": m / ((mean["build_ms"] + tck) / 1e3),
+            "deeper": deeper,
             "work": {"wedges": st["wedges"], "q_out": st["q_out"], "q_in": st["q_in"],
                      "max_out_degree": st["max_out_degree"], "max_degree": st["max_degree"],
                      "peel_rounds_last": st["peel_rounds"]},
