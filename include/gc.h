@@ -24,8 +24,9 @@
  *    is synchronised before return).
  *  - Call order: gc_create -> [gc_comm_init | gc_comm_init_loopback] ->
  *    gc_load_edges -> gc_build_csr -> any of gc_triangle_count,
- *    gc_edge_support, gc_ktruss, gc_truss_decomposition, gc_get_edges, any
- *    number of times.  A call out of order returns GC_ERR_STATE.
+ *    gc_edge_support, gc_ktruss, gc_ktruss_analysis, gc_truss_decomposition,
+ *    gc_list_triangles, gc_get_edges, any number of times.  A call out of
+ *    order returns GC_ERR_STATE.
  *    gc_load_edges invalidates the built graph.
  *  - Edge ids: the canonical edge list is the set of undirected edges
  *    {min(u,v), max(u,v)} with u != v, sorted lexicographically; edge id =
