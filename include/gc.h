@@ -184,7 +184,8 @@ int gc_truss_decomposition(gc_ctx* ctx, int32_t* trussness_out, int32_t* kmax);
 typedef enum gc_option {
     GC_OPT_FORCE_CLASS = 1,   /* -1 auto; 0..3 force every oriented edge through one
                                  intersection kernel class */
-    GC_OPT_TASK_CHUNK = 2,    /* wedge budget per intersection task (default 4096) */
+    GC_OPT_TASK_CHUNK = 2,    /* cost budget per intersection task, in units of one wedge
+                                 plus 128 per in-edge (default 32768; 8x for block tasks) */
     GC_OPT_TIMING = 3,        /* 1: record CUDA events per phase (default 1) */
     GC_OPT_LONG_SEG = 5,      /* suffixes at least this long take the warp-vector path
                                  (default 48; 2^30 disables it; testing) */

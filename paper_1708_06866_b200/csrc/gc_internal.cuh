@@ -67,7 +67,7 @@ struct gc_ctx {
 
     // options
     int force_class = -1;
-    int64_t task_chunk = 4096;
+    int64_t task_chunk = 32768;
     int timing = 1;
     int block_bitmap = 1;
     int long_seg = 48;

@@ -39,7 +39,10 @@ namespace gcx {
 namespace {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
-constexpr int kOvh = 2;                     // per in-edge overhead in the cost model
+#ifndef GC_KOVH
+#define GC_KOVH 128
+#endif
+constexpr int kOvh = GC_KOVH;               // per in-edge overhead in the cost model (cost units)
 #ifndef GC_KD1
 #define GC_KD1 128
 #endif

@@ -355,7 +355,7 @@ def test_heavy_head_bitmap_and_hash(ctx, gcmod, bitmap):
     finally:
         ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
         ctx.set_option(gcmod.GC_OPT_BLOCK_BITMAP, 1)
-        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 32768)
 
 
 @pytest.mark.parametrize("huge_max", [0, 40, 8192])
@@ -378,7 +378,7 @@ def test_huge_head_hash_and_global_probe(ctx, gcmod, huge_max):
     finally:
         ctx.set_option(gcmod.GC_OPT_FORCE_CLASS, -1)
         ctx.set_option(gcmod.GC_OPT_HUGE_MAX, 8192)
-        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 32768)
 
 
 def test_task_chunk_sizes(ctx, gcmod):
@@ -391,7 +391,7 @@ def test_task_chunk_sizes(ctx, gcmod):
             run_gpu(ctx, u, v)
             assert np.array_equal(ctx.edge_support(), want)
     finally:
-        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 4096)
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 32768)
 
 
 def test_large_clique_all_classes(ctx):
