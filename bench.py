@@ -326,6 +326,7 @@ def main():
     # ---- deeper trusses and the decomposition on the same graph (reported, not the step)
     deeper = {}
     if not args.no_extra:
+        ctx.ktruss_analysis(4, sup_out, mask_out)          # first peel with rounds: row buffers allocated
         for kk in (4, 5, 6):
             t = timed(lambda: ctx.ktruss_analysis(kk, sup_out, mask_out), 1)
             deeper[f"ktruss_analysis_k{kk}_ms"] = t
