@@ -75,10 +75,10 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #endif
 #define GC_HUGE_WARPS(S) ((S) ? GC_HUGE_WARPS_SUP : GC_HUGE_WARPS_TC)
 #ifndef GC_TC_WARPS
-#define GC_TC_WARPS 8                       // heavy-head count kernel: warps per block
+#define GC_TC_WARPS 10                      // heavy-head count kernel: warps per block
 #endif
 #ifndef GC_TC_MINB
-#define GC_TC_MINB 6
+#define GC_TC_MINB 5
 #endif
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
