@@ -50,7 +50,7 @@ constexpr int kD0 = 8, kD1 = GC_KD1, kD2 = 4096;    // class bounds on d+(v)
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 constexpr int kTS1 = pow2_at_least(2 * kD1);   // class-1 warp hash slots: load <= 1/2 at d+ = kD1
 static_assert((kTS1 & (kTS1 - 1)) == 0 && kTS1 >= 2 * kD1, "class-1 table: power of two, load <= 1/2");
-constexpr int64_t kTinyChunk = 256;   // class-0 task budget: one task per lane, keep lanes even
+constexpr int64_t kTinyChunk = 1024;  // class-0 task budget (cost units): one task per lane, keep lanes even
 #ifndef GC_TINY_IN
 #define GC_TINY_IN 64
 #endif

@@ -1,2 +1,2 @@
-for L in k64 k96 k192; do echo $L; GC_LIB_PATH=exp/libgc_$L.so timeout 600 python scripts/tune.py C4 "long_seg=48" 2>&1 | tail -1; done
-echo k128; timeout 600 python scripts/tune.py C4 "long_seg=48" 2>&1 | tail -1
+for C in K13 C4 C2; do timeout 600 python scripts/tune.py $C "long_seg=48" 2>&1 | tail -1; done
+timeout 900 python -m pytest tests -m gpu -x -q -p no:warnings -k "c1 or c2 or king or golden" 2>&1 | tail -1
