@@ -730,10 +730,13 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
     GC_TRY(host_scratch(c, 4096));
     GC_TRY(record(c, 0));
     GC_TRY(support_dag(c));                 // cold: support computed inside every call
-    if (triangles) {                        // the support pass found every triangle once
+    {                                       // the support pass found every triangle once
         unsigned long long* hits = support_hits(c);
+        // collective on every rank whatever the output pointers (SPMD callers may differ in NULLs)
         if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(hits), 1));
-        GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 512, hits, 8, cudaMemcpyDeviceToHost, c->stream));
+        if (triangles)
+            GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 512, hits, 8, cudaMemcpyDeviceToHost,
+                                       c->stream));
     }
     if (support_out && m > 0) {             // supports before the peel consumes them
         GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
@@ -742,7 +745,7 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
     }
     GC_TRY(record(c, 2));
     int64_t removed = 0;
-    if (alive_out || m_alive) {
+    if (alive_out || m_alive || c->nccl) {   // the peel is collective under a communicator
         GC_TRY(peel_setup(c));
         if (m > 0 && k > 2) {
             int32_t round = 0;
