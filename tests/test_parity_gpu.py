@@ -262,8 +262,15 @@ def test_c4_full_size_sampled(gcmod):
         sup = c.edge_support()
         cu, cv = c.get_edges()
         mask, m_alive = c.ktruss(3)
+        # bench.py's step: the fused call, device output buffers on torch's stream
+        dsup = torch.empty(m, dtype=torch.int32, device="cuda")
+        dmask = torch.empty(m, dtype=torch.uint8, device="cuda")
+        T2, _, _, m_alive2 = c.ktruss_analysis(3, dsup, dmask)
     finally:
         c.close()
+    assert T2 == T and m_alive2 == m_alive
+    assert np.array_equal(dsup.cpu().numpy().view(np.uint32), sup)
+    assert np.array_equal(dmask.cpu().numpy(), mask)
     assert int(sup.astype(np.int64).sum()) == 3 * T
     g = oracle.OracleGraph(u, v)
     assert g.m == m
