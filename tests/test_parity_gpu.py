@@ -164,6 +164,58 @@ def test_random_small_graphs(ctx):
         check_all(ctx, u, v, ks=(2, 3, 4, 5, 6))
 
 
+def test_fuzz_mixed_structures_and_options(gcmod):
+    """Seeded fuzz: planted cliques on a sparse random background with hubs,
+    duplicates, reversed pairs, self loops and isolated high ids; every
+    result (count, supports, k-truss at random k, decomposition, fused call,
+    listing count) against the oracle, under randomly drawn kernel options
+    (forced class, task chunk, bitmap, huge-hash limit, long-segment
+    threshold, compaction, partitioned peeler, loopback partitions)."""
+    rng = np.random.default_rng(2026)
+    for trial in range(40):
+        n = int(rng.integers(20, 400))
+        u, v = random_graph(n, float(rng.uniform(0.01, 0.08)), rng)
+        parts_u, parts_v = [u], [v]
+        for _ in range(int(rng.integers(1, 4))):              # planted cliques (deep trusses)
+            q = rng.choice(n, size=int(rng.integers(4, min(n, 40))), replace=False).astype(np.int32)
+            a, b = np.triu_indices(q.size, 1)
+            parts_u.append(q[a]); parts_v.append(q[b])
+        hub = int(rng.integers(0, n))                          # a hub joined to a third of the vertices
+        nb = rng.choice(n, size=n // 3, replace=False).astype(np.int32)
+        parts_u.append(np.full(nb.size, hub, np.int32)); parts_v.append(nb)
+        u = np.concatenate(parts_u); v = np.concatenate(parts_v)
+        dup = rng.choice(u.size, size=u.size // 5)             # duplicates, both orientations, loops
+        u = np.concatenate([u, v[dup], u[:7], np.array([n + 5], np.int32)])
+        v = np.concatenate([v, u[dup], u[:7], np.array([n + 9], np.int32)])   # isolated edge far out
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            loop = int(rng.choice([0, 0, 2, 3]))
+            if loop:
+                c.comm_init_loopback(loop)
+            opts = {gcmod.GC_OPT_TASK_CHUNK: int(rng.choice([64, 777, 32768])),
+                    gcmod.GC_OPT_LONG_SEG: int(rng.choice([8, 48, 1 << 30])),
+                    gcmod.GC_OPT_BLOCK_BITMAP: int(rng.integers(0, 2)),
+                    gcmod.GC_OPT_HUGE_MAX: int(rng.choice([0, 16, 8192])),
+                    gcmod.GC_OPT_COMPACT: int(rng.choice([0, 2, 3])),
+                    gcmod.GC_OPT_PEEL_PART: int(rng.integers(0, 2)),
+                    gcmod.GC_OPT_FORCE_CLASS: int(rng.choice([-1, -1, 1, 2, 3]))}
+            c.load_edges(u, v)
+            for o, val in opts.items():
+                c.set_option(o, val)
+            c.build_csr()
+            assert c.triangle_count() == g.triangle_count(), (trial, opts)
+            assert np.array_equal(c.edge_support(), g.support()), (trial, opts)
+            k = int(rng.integers(3, 12))
+            want, _ = g.ktruss(k)
+            assert np.array_equal(c.ktruss(k)[0], want), (trial, k, opts)
+            T, sup, mask, ma = c.ktruss_analysis(k)
+            assert T == g.triangle_count() and np.array_equal(sup, g.support()) and np.array_equal(mask, want)
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax = g.truss_decomposition()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax, (trial, opts)
+            assert len(c.list_triangles()) == g.triangle_count()
+
+
 def test_rmat_small_full(ctx):
     for s, ef, seed in [(8, 8, 5), (11, 16, 6), (12, 4, 7)]:
         u, v = gen.rmat(s, ef, seed=seed)
