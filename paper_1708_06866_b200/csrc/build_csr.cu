@@ -128,15 +128,22 @@ __global__ void k_orient(const uint64_t* __restrict__ canon, int64_t m, int b, c
     }
 }
 
-__global__ void k_split_keys(const uint64_t* __restrict__ keys, int64_t m, int b, int32_t* __restrict__ lo_out,
-                             int32_t* __restrict__ hi_out) {
+// split of the sorted oriented keys fused with the row bounds of the CSR
+// (first / last position of each row, rows = high part)
+__global__ void k_split_keys_bounds(const uint64_t* __restrict__ keys, int64_t m, int b, int32_t* __restrict__ col,
+                                    int32_t* __restrict__ row, int32_t* __restrict__ first,
+                                    int32_t* __restrict__ last) {
     const uint64_t mask = (1ULL << b) - 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t k = keys[i];
-        hi_out[i] = (int32_t)(k >> b);   // row id (high part)
-        lo_out[i] = (int32_t)(k & mask); // column (low part)
+        const uint64_t k = keys[i];
+        const int32_t r = (int32_t)(k >> b);
+        row[i] = r;
+        col[i] = (int32_t)(k & mask);
+        if (i == 0 || (int32_t)(keys[i - 1] >> b) != r) first[r] = (int32_t)i;
+        if (i == m - 1 || (int32_t)(keys[i + 1] >> b) != r) last[r] = (int32_t)(i + 1);
     }
 }
+
 
 // CSR row pointers from a row-sorted COO row array, in three parallel steps
 // (no thread walks a gap of empty rows): each run of equal rows records its
@@ -164,14 +171,19 @@ __global__ void k_pos_tail(const int32_t* __restrict__ dag_src, int64_t m, uint6
         vals[p] = ((uint64_t)(uint32_t)dag_src[p] << 32) | (uint64_t)(uint32_t)p;
 }
 
-__global__ void k_split_pos_tail(const uint64_t* __restrict__ vals, int64_t m, int32_t* __restrict__ pos,
-                                 int32_t* __restrict__ tail) {
+__global__ void k_split_pos_tail_bounds(const uint64_t* __restrict__ vals, const int32_t* __restrict__ head, int64_t m,
+                                        int32_t* __restrict__ pos, int32_t* __restrict__ tail,
+                                        int32_t* __restrict__ first, int32_t* __restrict__ last) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t x = vals[i];
         pos[i] = (int32_t)(uint32_t)x;
         tail[i] = (int32_t)(x >> 32);
+        const int32_t r = head[i];
+        if (i == 0 || head[i - 1] != r) first[r] = (int32_t)i;
+        if (i == m - 1 || head[i + 1] != r) last[r] = (int32_t)(i + 1);
     }
 }
+
 
 // Work-model sums over vertices: wedges = Σ C(d+,2), Q_out = Σ d+², Q_in = Σ d- d+,
 // max d+, max d.
@@ -237,6 +249,19 @@ static int csr_ptr_from_sorted(gc_ctx* c, const int32_t* row, int64_t m, int64_t
     int64_t* len = c->keys_b.as<int64_t>();
     GC_CUDA(c, cudaMemsetAsync(first, 0, (size_t)n * 8, c->stream));
     if (m > 0) GC_LAUNCH(c, k_run_bounds, grid_for(m), kThreads, 0, row, m, first, last);
+    GC_LAUNCH(c, k_row_len, grid_for(n + 1), kThreads, 0, first, last, n, len);
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, ptr, n + 1, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, len, ptr, n + 1, c->stream));
+    c->stats.lib_launches += 2;
+    return GC_OK;
+}
+
+// row pointers from first / last bounds already written (rows without entries: first = last = 0)
+static int ptr_from_bounds(gc_ctx* c, const int32_t* first, const int32_t* last, int64_t n, int64_t* len,
+                           int64_t* ptr) {
     GC_LAUNCH(c, k_row_len, grid_for(n + 1), kThreads, 0, first, last, n, len);
     size_t tmp = 0;
     GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, ptr, n + 1, c->stream));
@@ -399,10 +424,19 @@ int build_csr(gc_ctx* c) {
                   c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
         GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
                           c->dag_eid.as<int32_t>(), m, 2 * b));
-        GC_LAUNCH(c, k_split_keys, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b, c->dag_col.as<int32_t>(),
-                  c->dag_src.as<int32_t>());
     }
-    GC_TRY(csr_ptr_from_sorted(c, c->dag_src.as<int32_t>(), m, n, c->dag_ptr.as<int64_t>()));
+    {
+        // split the sorted keys into (dag_col, dag_src) and the row bounds in one pass;
+        // keys_a is free after the sort: first / last there, row lengths in vals_a
+        int32_t* first = reinterpret_cast<int32_t*>(c->keys_a.p);
+        int32_t* last = first + n;
+        GC_CUDA(c, cudaMemsetAsync(first, 0, (size_t)n * 8, c->stream));
+        if (m > 0)
+            GC_LAUNCH(c, k_split_keys_bounds, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, b,
+                      c->dag_col.as<int32_t>(), c->dag_src.as<int32_t>(), first, last);
+        GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+        GC_TRY(ptr_from_bounds(c, first, last, n, c->tmp_a.as<int64_t>(), c->dag_ptr.as<int64_t>()));
+    }
     // in-lists: sort (head, tail) with the DAG position as payload
     if (m > 0) {
         // DAG order is sorted by (tail, head): a stable sort on the head alone
@@ -418,10 +452,16 @@ int build_csr(gc_ctx* c) {
         tmp = c->cub_tmp.cap;
         GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hk, hk_out, pv, pv_out, m, 0, b, c->stream));
         c->stats.lib_launches += 2 + (b + 7) / 8;
-        GC_LAUNCH(c, k_split_pos_tail, grid_for(m), kThreads, 0, pv_out, m, c->in_pos.as<int32_t>(),
-                  c->in_src.as<int32_t>());
+        int32_t* first = reinterpret_cast<int32_t*>(c->keys_a.p);   // pv (keys_a) consumed by the sort
+        int32_t* last = first + n;
+        GC_CUDA(c, cudaMemsetAsync(first, 0, (size_t)n * 8, c->stream));
+        GC_LAUNCH(c, k_split_pos_tail_bounds, grid_for(m), kThreads, 0, pv_out, c->in_dst.as<int32_t>(), m,
+                  c->in_pos.as<int32_t>(), c->in_src.as<int32_t>(), first, last);
+        GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+        GC_TRY(ptr_from_bounds(c, first, last, n, c->tmp_a.as<int64_t>(), c->in_ptr.as<int64_t>()));
+    } else {
+        GC_TRY(csr_ptr_from_sorted(c, c->in_dst.as<int32_t>(), m, n, c->in_ptr.as<int64_t>()));
     }
-    GC_TRY(csr_ptr_from_sorted(c, c->in_dst.as<int32_t>(), m, n, c->in_ptr.as<int64_t>()));
 
     // ---- work-model statistics (one reduction over vertices)
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 512);

@@ -126,24 +126,34 @@ __global__ void k_in_cost(const int32_t* __restrict__ in_pos, const int32_t* __r
     }
 }
 
+// Per head v: the cost budget of its tasks (0 when v has no work): 8x the
+// chunk for block classes, the tiny budget for lane tasks.
+__global__ void k_head_chunk(const int64_t* __restrict__ pref, const int64_t* __restrict__ in_ptr,
+                             const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col, int64_t n,
+                             int64_t chunk, int force, uint32_t bm_bits, int64_t* __restrict__ hch) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ch = 0;
+        if (dag_ptr[v + 1] > dag_ptr[v] && pref[in_ptr[v + 1]] > pref[in_ptr[v]]) {
+            const int cl = head_class(dag_ptr, dag_col, in_ptr, (int)v, force, bm_bits);
+            ch = cl >= 2 ? chunk * kWarps : cl == 0 ? min(chunk, kTinyChunk) : chunk;
+        }
+        hch[v] = ch;
+    }
+}
+
 // A task starts at the first in-edge of every head v that has work, and
-// wherever the running cost crosses a multiple of the class's chunk or an
+// wherever the running cost crosses a multiple of the head's budget or an
 // owner boundary (multi-GPU cut).  Zero-cost in-edges (empty suffix) stay
 // inside the surrounding task.
 __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __restrict__ in_dst,
-                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ dag_ptr,
-                             const int32_t* __restrict__ dag_col, int64_t m, int64_t chunk, int64_t total, int parts,
-                             int force, uint32_t bm_bits, uint8_t* __restrict__ flag) {
+                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ hch, int64_t m,
+                             int64_t total, int parts, uint8_t* __restrict__ flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int v = in_dst[i];
-        const int64_t s = in_ptr[v], e = in_ptr[v + 1];
-        const int64_t dv = dag_ptr[v + 1] - dag_ptr[v];
+        const int64_t ch = hch[v];
         uint8_t f = 0;
-        if (dv > 0 && pref[e] > pref[s]) {
-            // block-class tasks get 8x the budget (8 warps share one table)
-            const int cl = head_class(dag_ptr, dag_col, in_ptr, v, force, bm_bits);
-            const int64_t ch = cl >= 2 ? chunk * kWarps : cl == 0 ? min(chunk, kTinyChunk) : chunk;
-            if (i == s) f = 1;
+        if (ch > 0) {
+            if (i == in_ptr[v]) f = 1;
             else if (pref[i] / ch != pref[i - 1] / ch) f = 1;
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
         }
@@ -728,9 +738,13 @@ int prepare_tasks(gc_ctx* c) {
         return GC_OK;
     }
     uint8_t* flags = reinterpret_cast<uint8_t*>(c->vals_b.p);
+    GC_TRY(ensure(c, c->keys_b, (size_t)(c->n + 1) * 8));
+    int64_t* hch = c->keys_b.as<int64_t>();                 // free after the build
+    GC_LAUNCH(c, k_head_chunk, grid_for(c->n), kThreads, 0, c->in_cost.as<int64_t>(), c->in_ptr.as<int64_t>(),
+              c->dag_ptr.as<int64_t>(), c->dag_col.as<int32_t>(), c->n, c->task_chunk, c->force_class, bm_bits_of(c),
+              hch);
     GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(),
-              c->in_ptr.as<int64_t>(), c->dag_ptr.as<int64_t>(), c->dag_col.as<int32_t>(), m, c->task_chunk,
-              c->total_cost, c->task_parts, c->force_class, bm_bits_of(c), flags);
+              c->in_ptr.as<int64_t>(), hch, m, c->total_cost, c->task_parts, flags);
     int32_t* sel = c->vals_a.as<int32_t>();
     int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 128);
     thrust::counting_iterator<int32_t> iota(0);
