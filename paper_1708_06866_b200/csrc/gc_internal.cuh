@@ -61,6 +61,7 @@ struct gc_ctx {
     cudaStream_t side = nullptr;     // library-owned side stream (warp-task classes overlap the block kernels)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int overlap = 1;                 // GC_OPT_OVERLAP
+    int launch_grid[4][2] = {};      // intersection kernels: occupancy grid per class and SUP (0: not yet set up)
     std::string err;
     bool poisoned = false;
     int state = 0;  // 0 created, 1 edges loaded, 2 graph built

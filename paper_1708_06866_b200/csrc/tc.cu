@@ -817,57 +817,50 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         GC_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
         GC_CUDA(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     }
+    // Per-context launch cache (the context is bound to one device; the
+    // shared-memory opt-in and the occupancy grid are per device and kernel).
+    auto prep = [&](int slot, auto kernel, size_t smem, int threads) -> int {
+        int& g = c->launch_grid[slot][SUP];
+        if (g == 0) {
+            if (smem > 48 * 1024 &&
+                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return -1;
+            g = occupancy_grid(kernel, smem, threads);
+        }
+        return g;
+    };
     // classes 3 and 2 first (heaviest tasks), then 1, 0
     if (c->ntask[3] > 0) {
         a.tasks = tasks + c->task_off[3];
         a.ntask = c->ntask[3];
         const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
-        static bool attr_set[2] = {false, false};
-        if (!attr_set[SUP]) {
-            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
-            attr_set[SUP] = true;
-        }
         constexpr int threads = 32 * GC_HUGE_WARPS(SUP);
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_block<SUP, true>, smem, threads);
+        const int grid = prep(3, k_tc_block<SUP, true>, smem, threads);
+        if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block huge)", __FILE__, __LINE__);
         GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
     }
     if (c->ntask[2] > 0) {
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
-        static bool attr_set[2] = {false, false};
-        if (!attr_set[SUP]) {
-            GC_CUDA(c, cudaFuncSetAttribute(k_tc_block<SUP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
-            attr_set[SUP] = true;
-        }
         constexpr int threads = 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS);
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_block<SUP, false>, smem, threads);
+        const int grid = prep(2, k_tc_block<SUP, false>, smem, threads);
+        if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block)", __FILE__, __LINE__);
         GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
     }
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
         a.ntask = c->ntask[1];
         const size_t smem = kWarps * (SUP ? 3 * kTS1 : kTS1) * sizeof(uint32_t);
-        static bool attr_set = false;
-        if (!attr_set) {
-            GC_CUDA(c, cudaFuncSetAttribute(k_tc_warp<kTS1, SUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
-            attr_set = true;
-        }
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_warp<kTS1, SUP>, smem);
+        const int grid = prep(1, k_tc_warp<kTS1, SUP>, smem, 256);
+        if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_warp)", __FILE__, __LINE__);
         GC_LAUNCH_S(c, ws, (k_tc_warp<kTS1, SUP>), (int)std::min<int64_t>(grid, (a.ntask + kWarps - 1) / kWarps), 256,
                     smem, a);
     }
     if (c->ntask[0] > 0) {
         a.tasks = tasks + c->task_off[0];
         a.ntask = c->ntask[0];
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(k_tc_tiny<SUP>, 0);
+        const int grid = prep(0, k_tc_tiny<SUP>, 0, 256);
         GC_LAUNCH_S(c, ws, (k_tc_tiny<SUP>), (int)std::min<int64_t>(grid, (a.ntask + 255) / 256), 256, 0, a);
     }
     if (fork) {
