@@ -252,6 +252,20 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
                     const uint32_t h4 = probe.hit((uint32_t)V.x) | (probe.hit((uint32_t)V.y) << 1) |
                                         (probe.hit((uint32_t)V.z) << 2) | (probe.hit((uint32_t)V.w) << 3);
                     seg_hits += __popc(h4 & in4);
+                } else if (Probe::kBranchFree) {
+                    // support, bitmap probe: the four probes first (independent
+                    // loads the compiler cannot move past the credits' shared
+                    // atomics, which might alias), then the hits
+                    const int h0 = probe.loc((uint32_t)V.x), h1 = probe.loc((uint32_t)V.y),
+                              h2 = probe.loc((uint32_t)V.z), h3 = probe.loc((uint32_t)V.w);
+                    auto take = [&](int q, int hd) {
+                        if ((uint32_t)(q - b) < (uint32_t)(e - b) && hd >= 0) {
+                            ++seg_hits;
+                            if (!(uw & 2)) probe.credit(hd, sup);     // role (v,w)
+                            if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
+                        }
+                    };
+                    take(q0, h0); take(q0 + 1, h1); take(q0 + 2, h2); take(q0 + 3, h3);
                 } else {
                     visit(q0, V.x); visit(q0 + 1, V.y); visit(q0 + 2, V.z); visit(q0 + 3, V.w);
                 }
@@ -325,6 +339,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
 // index j within N+(v), cnt = (v,w)-role credits.
 template <bool SUP>
 struct SmemHash {
+    static constexpr bool kBranchFree = false;
     uint32_t* keys;
     int32_t* vals;
     uint32_t* cnt;
@@ -482,6 +497,7 @@ __global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
 
 template <bool SUP>
 struct SmemBitmap {
+    static constexpr bool kBranchFree = true;   // loc() is one LDS, no probe chain
     const uint32_t* bits;    // == g_dsmem (word 0 of the dynamic shared memory)
     const uint16_t* pre;     // SUP: index in N+(v) of the first element of each 64-bit chunk
     uint32_t* cnt;           // SUP: (v,w)-role credits per index j
@@ -533,6 +549,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* __restrict__ 
 
 // Probe of N+(v) in global memory (binary search): huge heads past the table.
 struct GlobalProbe {
+    static constexpr bool kBranchFree = false;
     const int32_t* row;
     int d;
     int64_t r0;

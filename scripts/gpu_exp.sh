@@ -1,1 +1,2 @@
-for L in sw9 sw11; do echo $L; GC_LIB_PATH=exp/libgc_$L.so timeout 600 python scripts/tune.py C4 "long_seg=48" 2>&1 | tail -1; done
+timeout 600 python scripts/tune.py C4 "long_seg=48" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q -p no:warnings -k "forced or heavy or c3 or c1 or fuzz" 2>&1 | tail -1
