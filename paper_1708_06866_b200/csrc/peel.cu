@@ -21,6 +21,8 @@
 // until X is empty (fixed point).  Decomposition: k = 3, 4, ...
 // continue from the previous k's survivors; edges removed at level k get
 // trussness k-1.
+#include <cuda_profiler_api.h>
+
 #include <algorithm>
 #include <cstring>
 
@@ -322,6 +324,32 @@ __global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int nfront = A.nfront_dev ? *A.nfront_dev : A.nfront;
+    if (nfront > 0 && 2 * (int64_t)nfront <= warps) {
+        // Few frontier edges (the late rounds of the dense cores: a handful of
+        // edges with long rows): each edge's shorter row is cut into wpe
+        // 32-aligned slices, one per warp, so the whole grid works on them
+        // instead of one warp per edge.  No early exit (S(e) counts the edge's
+        // triangles across all slices); each triangle is still met once, in
+        // the slice holding its entry of the shorter row.
+        const int64_t wpe = warps / nfront;
+        const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+        const int64_t ei = wid / wpe, slice = wid % wpe;
+        if (ei >= nfront) return;
+        const int e = A.front[ei];
+        const uint32_t live = pol.live(e);
+        if (live == 0) return;
+        const int a = A.dag_src[e], b = A.dag_col[e];
+        int64_t a0 = A.sym_ptr[a], a1 = a0 + A.live_len[a], b0 = A.sym_ptr[b], b1 = b0 + A.live_len[b];
+        if (a1 - a0 > b1 - b0) {
+            int64_t t0 = a0, t1 = a1;
+            a0 = b0; a1 = b1; b0 = t0; b1 = t1;
+        }
+        const int64_t chunks = (a1 - a0 + 31) / 32;
+        const int64_t c0 = chunks * slice / wpe, c1 = chunks * (slice + 1) / wpe;
+        if (c1 > c0)
+            peel_one_warp(A, pol, e, 0xFFFFFFFFu, a0 + 32 * c0, min(a1, a0 + 32 * c1), b0, b1, lane);
+        return;
+    }
     const int G = (int)max((int64_t)1, min((int64_t)GC_PEEL_GMAX, nfront / warps));     // edges per warp
     for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G; base < nfront;
          base += warps * G) {
@@ -552,6 +580,14 @@ static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
 // level >= 0: write tau = level for removed edges.  Returns removed count.
 static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed) {
     const int64_t m = c->m;
+    // diagnostics: GC_PROFILE_LEVEL=<k-1> brackets that level with the CUDA
+    // profiler start/stop (ncu --profile-from-start off)
+    static const int prof_level = getenv("GC_PROFILE_LEVEL") ? atoi(getenv("GC_PROFILE_LEVEL")) : -2;
+    struct ProfScope {
+        bool on;
+        ~ProfScope() { if (on) cudaProfilerStop(); }
+    } prof{prof_level == level};
+    if (prof.on) cudaProfilerStart();
     int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
     int32_t* h = static_cast<int32_t*>(c->hpin);
     *removed = 0;
