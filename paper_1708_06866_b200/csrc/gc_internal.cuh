@@ -135,7 +135,7 @@ struct gc_ctx {
     int64_t alist_n = -1;       // -1: no list (scan every edge)
     int64_t m_alive_h = 0;      // live edges (host mirror)
     int64_t compact_at = 0;     // live edges at the last compaction
-    int trace = getenv("GC_PEEL_TRACE") != nullptr;   // diagnostics: one stderr line per peel round
+    int trace = getenv("GC_PEEL_TRACE") ? atoi(getenv("GC_PEEL_TRACE")) : 0;   // diagnostics: 1 a line per batch, 2 per round
     int compact_div = 2;        // compact when live edges fall to 1/compact_div (GC_OPT_COMPACT; <= 1 never)
     gcx::Buf alive;     // uint8[m]
     gcx::Buf rem;       // int32[m] round in which the edge is in the frontier

@@ -622,7 +622,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 256);   // removed, rounds
     GC_CUDA(c, cudaMemsetAsync(acc, 0, 16, c->stream));
     const int64_t alive0 = c->m_alive_h;
-    int cur = 0, batch = 2;
+    int cur = 0, batch = c->trace > 1 ? 1 : 2;   // GC_PEEL_TRACE=2: one round per batch (per-round trace)
     unsigned long long done[2] = {0, 0};
     while (nf > 0) {
         GC_TRY(record(c, 8));
@@ -646,12 +646,12 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         c->stats.peel_kernel_ms += elapsed(c, 8, 9);
         memcpy(done, h + 2, 16);
         if (c->trace)
-            fprintf(stderr, "peel-trace level %d batch %d rounds %llu removed %llu ms %.4f\n", level, batch, done[1],
-                    done[0], elapsed(c, 8, 9));
+            fprintf(stderr, "peel-trace level %d batch %d nf %d rounds %llu removed %llu ms %.4f\n", level, batch, nf,
+                    done[1], done[0], elapsed(c, 8, 9));
         c->m_alive_h = alive0 - (int64_t)done[0];
         nf = h[0];
         if (nf > 0) GC_TRY(maybe_compact(c));
-        batch = std::min(batch * 2, 16);
+        if (c->trace < 2) batch = std::min(batch * 2, 16);
     }
     *removed += (int64_t)done[0];
     c->stats.peel_rounds += (int64_t)done[1];
