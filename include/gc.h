@@ -209,6 +209,12 @@ typedef enum gc_option {
     GC_OPT_OVERLAP = 13,      /* 1: the warp-task intersection kernels run on a library
                                  side stream that overlaps the block-task kernels and is
                                  joined before the call returns (default); 0: one stream */
+    GC_OPT_GROUP_PEEL = 12,   /* peeler: rounds with at least this many frontier edges
+                                 (default 2^20; 0: never) -- a dense core collapsing -- group
+                                 their heavy edges by the endpoint with the longer live row,
+                                 whose row is staged once per group as a shared-memory bitmap */
+    GC_OPT_GROUP_HEAVY = 14,  /* ... heavy = shorter live row at least this long (default
+                                 1024); lighter edges keep the per-edge search */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

@@ -131,14 +131,16 @@ struct gc_ctx {
     gcx::Buf live_len;  // int32[n] live entries at the front of each symmetric row
     gcx::Buf long_rows; // int32 rows longer than kLongRow (compacted block-wide)
     int nlong = 0;
+    gcx::Buf grp_keys, grp_vals, grp_starts, grp_flags, grp_light;   // grouped dense-core rounds
+    int group_peel = 1 << 20;   // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
+    int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped
     gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)
     int64_t alist_n = -1;       // -1: no list (scan every edge)
     int64_t m_alive_h = 0;      // live edges (host mirror)
     int64_t compact_at = 0;     // live edges at the last compaction
     int trace = getenv("GC_PEEL_TRACE") ? atoi(getenv("GC_PEEL_TRACE")) : 0;   // diagnostics: 1 a line per batch, 2 per round
     int compact_div = 2;        // compact when live edges fall to 1/compact_div (GC_OPT_COMPACT; <= 1 never)
-    gcx::Buf alive;     // uint8[m]
-    gcx::Buf rem;       // int32[m] round in which the edge is in the frontier
+    gcx::Buf alive;     // uint8[m] edge state: 0 removed, 1 alive, 2 / 3 in the frontier (peel.cu st_front)
     gcx::Buf front_a, front_b;  // int32[m] frontier lists
     gcx::Buf tau;       // int32[m]
     gcx::Buf xbits;     // uint32 removed-edge bitmap X of the round (partitioned peel, allgathered)

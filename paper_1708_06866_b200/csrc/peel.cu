@@ -21,7 +21,10 @@
 // until X is empty (fixed point).  Decomposition: k = 3, 4, ...
 // continue from the previous k's survivors; edges removed at level k get
 // trussness k-1.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cuda_profiler_api.h>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cstring>
@@ -177,17 +180,27 @@ __global__ void k_alive_list(const uint8_t* __restrict__ alive, int64_t m, int32
     }
 }
 
+// Edge state, one byte per edge (the alive array): 0 removed, 1 alive, and
+// st_front(r) = 2 + (r & 1) alive and in the frontier X of round r.  Crossings
+// during round r are stamped st_front(r + 1), which no edge of round r's X
+// carries, and X turns 0 when the round finishes, so two values suffice and a
+// triangle visit reads one byte per other edge for both "alive" and "in X"
+// (5x less state than a separate int32 round stamp: the dense cores' states
+// stay in L2).
+__host__ __device__ __forceinline__ uint8_t st_front(int32_t round) { return (uint8_t)(2 + (round & 1)); }
+
 // X = {alive e : S(e) < thr}, over the live-edge list (list == nullptr: all e < m)
 // An edge below the threshold with S(e) = 0 lies in no live triangle, so it
 // is removed on the spot (nothing to destroy, nobody sees it in this round);
 // the others go to the frontier list for the peel kernel.
 __global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restrict__ alive,
                                 const int32_t* __restrict__ list, int64_t len, uint32_t thr,
-                                int32_t* __restrict__ rem, int32_t round, int32_t* __restrict__ front,
+                                int32_t round, int32_t* __restrict__ front,
                                 int* __restrict__ count, int32_t* __restrict__ tau, int32_t level,
-                                unsigned long long* __restrict__ zero_removed) {
+                                unsigned long long* __restrict__ zero_removed, uint32_t* __restrict__ min_rest) {
     const int lane = threadIdx.x & 31;
     unsigned zeros = 0;
+    uint32_t rest = 0xFFFFFFFFu;   // min S over the alive edges left out of the frontier
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = list ? (int64_t)list[i] : i;
         bool in = false;
@@ -199,11 +212,12 @@ __global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restr
                 ++zeros;
             } else {
                 in = se < thr;
+                if (!in) rest = min(rest, se);
             }
         }
         unsigned ballot = __ballot_sync(__activemask(), in);
         if (in) {
-            rem[e] = round;
+            alive[e] = st_front(round);
             // warp-aggregated append
             int leader = __ffs(ballot) - 1;
             int base = 0;
@@ -214,6 +228,8 @@ __global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restr
     }
     zeros = __reduce_add_sync(0xffffffffu, zeros);
     if (lane == 0 && zeros) atomicAdd(zero_removed, (unsigned long long)zeros);
+    rest = __reduce_min_sync(0xffffffffu, rest);
+    if (lane == 0 && rest != 0xFFFFFFFFu) atomicMin(min_rest, rest);
 }
 
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t lo, int64_t hi, int32_t x) {
@@ -228,18 +244,18 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a
 // least one edge in X is handled only by its smallest-id edge in X, which
 // decrements each surviving edge once.  The two policies differ in how X is
 // represented and which survivors a rank may decrement.
-struct PolicySingle {       // one rank: X = {rem == round}; crossings append to the next list
-    int32_t* rem;
+struct PolicySingle {       // one rank: X = {st == st_front(round)}; crossings append to the next list
+    uint8_t* st;            // the alive array (edge state, see st_front)
     uint32_t* S;
     uint32_t thr;
     int32_t round;
     int32_t* next;
     int* next_count;
     __device__ __forceinline__ uint32_t live(int e) const { return S[e]; }   // exact at round start
-    __device__ __forceinline__ bool in_x(int f) const { return rem[f] == round; }
+    __device__ __forceinline__ bool in_x(int f) const { return st[f] == st_front(round); }
     __device__ __forceinline__ void dec(int f) const {
         if (atomicSub(S + f, 1u) == thr) {
-            rem[f] = round + 1;
+            st[f] = st_front(round + 1);
             next[atomicAdd(next_count, 1)] = f;
         }
     }
@@ -394,6 +410,155 @@ __global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
                           __shfl_sync(0xffffffffu, a0, src), __shfl_sync(0xffffffffu, a1, src),
                           __shfl_sync(0xffffffffu, b0, src), __shfl_sync(0xffffffffu, b1, src), lane);
         }
+    }
+}
+
+
+// ------------------------------------- grouped heavy edges (dense-core rounds) --
+// When a dense core collapses, single rounds carry 10^6-10^7 frontier edges
+// whose endpoints both have thousands of live neighbours (C5 level 2,496:
+// rounds of 5-19 M edges, 2.8 s each with the per-edge search).  Such rounds
+// group their heavy edges (shorter live row >= heavy_row) by pivot x, the
+// endpoint with the longer row: a block stages N_live(x) once as a 32 KB
+// rank-window bitmap, each warp streams the other endpoint's row of one heavy
+// edge and probes it, and only the hits (the live triangles) search row x for
+// the third edge's id.  Light edges keep the per-edge search.
+constexpr int kGrpBits = 1 << 18;      // bitmap window (ranks)
+constexpr int kGrpChunk = 1024;        // heavy edges per group at most
+
+template <class Pol>
+__global__ void k_split_heavy(PeelArgs A, Pol pol, int heavy_row, uint32_t* __restrict__ hkey,
+                              int32_t* __restrict__ hval, int* __restrict__ hcount, int32_t* __restrict__ light,
+                              int* __restrict__ lcount) {
+    const int lane = threadIdx.x & 31;
+    const int nfront = A.nfront_dev ? *A.nfront_dev : A.nfront;
+    for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; i0 < nfront; i0 += gridDim.x * blockDim.x) {
+        const int i = i0 + lane;
+        int e = -1, x = 0;
+        bool heavy = false, lgt = false;
+        if (i < nfront) {
+            e = A.front[i];
+            if (pol.live(e)) {
+                const int a = A.dag_src[e], b = A.dag_col[e];
+                const int la = A.live_len[a], lb = A.live_len[b];
+                heavy = min(la, lb) >= heavy_row;
+                lgt = !heavy;
+                x = lb >= la ? b : a;
+            }
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, heavy), lb2 = __ballot_sync(0xffffffffu, lgt);
+        int hbase = 0, lbase = 0;
+        if (lane == 0) {
+            if (hb) hbase = atomicAdd(hcount, __popc(hb));
+            if (lb2) lbase = atomicAdd(lcount, __popc(lb2));
+        }
+        hbase = __shfl_sync(0xffffffffu, hbase, 0);
+        lbase = __shfl_sync(0xffffffffu, lbase, 0);
+        const unsigned below = (1u << lane) - 1;
+        if (heavy) {
+            const int o = hbase + __popc(hb & below);
+            hkey[o] = (uint32_t)x;
+            hval[o] = e;
+        }
+        if (lgt) light[lbase + __popc(lb2 & below)] = e;
+    }
+}
+
+__global__ void k_group_flags(const uint32_t* __restrict__ key, int nh, uint8_t* __restrict__ flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || key[i] != key[i - 1] || i % kGrpChunk == 0) ? 1 : 0;
+}
+
+constexpr size_t kGrpSmem = kGrpBits / 8 + kGrpBits / 64 * 4 + 64;   // bitmap + prefix per 64 ranks
+
+template <class Pol>
+__global__ void __launch_bounds__(256, 4) k_peel_grouped(PeelArgs A, Pol pol, const uint32_t* __restrict__ key,
+                                                         const int32_t* __restrict__ edges, int nh,
+                                                         const int32_t* __restrict__ starts,
+                                                         const int* __restrict__ ngroups) {
+    // bits: every entry of the pivot row x (dead ones too), offset from its
+    // first rank wb; pre[c]: entries below rank wb + 64 c, so the position of
+    // a hit in row x -- and the third edge's id -- needs no search.
+    extern __shared__ unsigned long long grp_smem[];
+    unsigned long long* bits = grp_smem;
+    uint32_t* pre = reinterpret_cast<uint32_t*>(bits + kGrpBits / 64);
+    int* s_ok = reinterpret_cast<int*>(pre + kGrpBits / 64);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = *ngroups;
+    for (int j = threadIdx.x; j < kGrpBits / 64; j += blockDim.x) bits[j] = 0ull;   // zero between groups
+    __syncthreads();
+    for (int gi = blockIdx.x; gi < G; gi += gridDim.x) {
+        const int g0 = starts[gi], g1 = gi + 1 < G ? starts[gi + 1] : nh;
+        const int x = (int)key[g0];
+        const int64_t xb = A.sym_ptr[x];
+        const int L = A.live_len[x];
+        const int32_t wb = A.sym_col[xb];
+        const int32_t span = A.sym_col[xb + L - 1] - wb;
+        const bool ok = span < kGrpBits;
+        if (ok) {
+            for (int i = threadIdx.x; i < L; i += blockDim.x) {
+                const uint32_t off = (uint32_t)(A.sym_col[xb + i] - wb);
+                atomicOr(bits + (off >> 6), 1ull << (off & 63));
+            }
+            __syncthreads();
+            // exclusive prefix of the chunk popcounts: 16 chunks per thread + a block scan
+            const int nch = (span >> 6) + 1;
+            const int c0 = threadIdx.x * (kGrpBits / 64 / 256);
+            uint32_t loc = 0;
+            if (c0 < nch)
+                for (int c = c0; c < c0 + kGrpBits / 64 / 256; ++c) loc += __popcll(bits[c]);
+            uint32_t inc = loc;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += t;
+            }
+            if (lane == 31) s_ok[1 + warp] = (int)inc;
+            __syncthreads();
+            uint32_t base = inc - loc;
+            for (int w = 0; w < warp; ++w) base += (uint32_t)s_ok[1 + w];
+            if (c0 < nch)
+                for (int c = c0; c < c0 + kGrpBits / 64 / 256; ++c) {
+                    pre[c] = base;
+                    base += __popcll(bits[c]);
+                }
+        }
+        __syncthreads();
+        for (int k = g0 + warp; k < g1; k += 8) {
+            const int e = edges[k];
+            const uint32_t live = pol.live(e);
+            const int a = A.dag_src[e], b = A.dag_col[e];
+            const int y = a == x ? b : a;
+            const int64_t y0 = A.sym_ptr[y], y1 = y0 + A.live_len[y];
+            if (!ok) {
+                peel_one_warp(A, pol, e, live, y0, y1, xb, xb + L, lane);
+                continue;
+            }
+            uint32_t found = 0;
+            for (int64_t q = y0; q < y1 && found < live; q += 32) {
+                const int64_t i = q + lane;
+                bool tri = false;
+                int f = -1, g = -1;
+                if (i < y1) {
+                    const uint32_t off = (uint32_t)(__ldg(A.sym_col + i) - wb);
+                    const unsigned long long word = off < (uint32_t)kGrpBits ? bits[off >> 6] : 0ull;
+                    if ((word >> (off & 63)) & 1ull) {
+                        f = __ldg(A.sym_eid + i);
+                        if (f != e && A.alive[f]) {
+                            const uint32_t pos = pre[off >> 6] + __popcll(word & ((1ull << (off & 63)) - 1));
+                            g = __ldg(A.sym_eid + xb + pos);
+                            tri = A.alive[g] != 0;
+                        }
+                    }
+                }
+                found += __popc(__ballot_sync(0xffffffffu, tri));
+                if (tri) destroy(pol, e, f, g);
+            }
+        }
+        __syncthreads();
+        if (ok)
+            for (int i = threadIdx.x; i < L; i += blockDim.x)
+                bits[(uint32_t)(A.sym_col[xb + i] - wb) >> 6] = 0ull;
+        __syncthreads();
     }
 }
 
@@ -576,9 +741,73 @@ static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
     return GC_OK;
 }
 
+
+// A dense-core round: light frontier edges by the per-edge search, heavy ones
+// grouped by pivot (k_peel_grouped).  front / nf on the host.
+template <class Pol>
+static int peel_round_grouped(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
+    GC_TRY(ensure(c, c->grp_keys, (size_t)nf * 4 * 2));
+    GC_TRY(ensure(c, c->grp_vals, (size_t)nf * 4 * 2));
+    GC_TRY(ensure(c, c->grp_starts, (size_t)nf * 4 + 4));
+    GC_TRY(ensure(c, c->grp_flags, (size_t)nf + 4));
+    GC_TRY(ensure(c, c->grp_light, (size_t)nf * 4 + 4));
+    uint32_t* k0 = c->grp_keys.as<uint32_t>();
+    uint32_t* k1 = k0 + nf;
+    int32_t* v0 = c->grp_vals.as<int32_t>();
+    int32_t* v1 = v0 + nf;
+    int* cnts = reinterpret_cast<int*>(c->scal.as<char>() + 304);   // heavy, light, groups
+    GC_CUDA(c, cudaMemsetAsync(cnts, 0, 3 * sizeof(int), c->stream));
+    PeelArgs A{front, nf, nullptr, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(), c->sym_ptr.as<int64_t>(),
+               c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
+               c->alive.as<uint8_t>()};
+    GC_LAUNCH(c, k_split_heavy<Pol>, grid_for(nf), kThreads, 0, A, pol, c->group_heavy, k0, v0, cnts,
+              c->grp_light.as<int32_t>(), cnts + 1);
+    PeelArgs Lt = A;
+    Lt.front = c->grp_light.as<int32_t>();
+    Lt.nfront = 0;
+    Lt.nfront_dev = cnts + 1;
+    GC_LAUNCH(c, k_peel<Pol>, 148 * 8, 256, 0, Lt, pol);
+    int32_t* h = static_cast<int32_t*>(c->hpin);
+    GC_CUDA(c, cudaMemcpyAsync(h + 8, cnts, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(sync(c));
+    const int nh = h[8];
+    if (nh == 0) return GC_OK;
+    const int kbits = std::max(1, ceil_log2_u64((uint64_t)c->n));
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, nh, 0, kbits, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, k0, k1, v0, v1, nh, 0, kbits, c->stream));
+    GC_LAUNCH(c, k_group_flags, grid_for(nh), kThreads, 0, k1, nh, c->grp_flags.as<uint8_t>());
+    thrust::counting_iterator<int32_t> iota(0);
+    tmp = 0;
+    GC_CUDA(c, cub::DeviceSelect::Flagged(nullptr, tmp, iota, c->grp_flags.as<uint8_t>(), c->grp_starts.as<int32_t>(),
+                                          cnts + 2, nh, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, c->grp_flags.as<uint8_t>(),
+                                          c->grp_starts.as<int32_t>(), cnts + 2, nh, c->stream));
+    c->stats.lib_launches += 4 + (kbits + 7) / 8;
+    GC_CUDA(c, cudaFuncSetAttribute(k_peel_grouped<Pol>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGrpSmem));
+    GC_LAUNCH(c, k_peel_grouped<Pol>, 148 * 4, 256, kGrpSmem, A, pol, k1, v1, nh, c->grp_starts.as<int32_t>(),
+              cnts + 2);
+    return GC_OK;
+}
+
 // Peel at threshold thr = k - 2 starting from the current alive set / S.
 // level >= 0: write tau = level for removed edges.  Returns removed count.
-static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed) {
+#ifndef GC_BATCH_MAX_FRONT
+#define GC_BATCH_MAX_FRONT 16384
+#endif
+constexpr int kBatchMaxFront = GC_BATCH_MAX_FRONT;
+
+// *next_thr (when non-null): with an empty frontier nothing but S = 0 edges
+// left, so no S changed and every threshold up to min S over the survivors
+// finds an empty frontier too -- the smallest threshold worth scanning next
+// (0: unknown, the frontier was not empty).  The decomposition jumps there
+// (C5: 757 non-empty levels of 2,873).
+static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed,
+                      uint32_t* next_thr) {
     const int64_t m = c->m;
     // diagnostics: GC_PROFILE_LEVEL=<k-1> brackets that level with the CUDA
     // profiler start/stop (ncu --profile-from-start off)
@@ -597,13 +826,16 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     const int64_t len = c->alist_n >= 0 ? c->alist_n : m;
     GC_TRY(record(c, 10));
     unsigned long long* zrem = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 240);
+    uint32_t* min_rest = reinterpret_cast<uint32_t*>(c->scal.as<char>() + 320);
     GC_CUDA(c, cudaMemsetAsync(zrem, 0, 8, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(min_rest, 0xFF, 4, c->stream));
     GC_LAUNCH(c, k_frontier_scan, grid_for(len), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), list,
-              len, thr, c->rem.as<int32_t>(), *round, c->front_a.as<int32_t>(), cnt,
-              level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem);
+              len, thr, *round, c->front_a.as<int32_t>(), cnt,
+              level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem, min_rest);
     GC_TRY(record(c, 11));
     GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     GC_CUDA(c, cudaMemcpyAsync(h + 2, zrem, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_CUDA(c, cudaMemcpyAsync(h + 4, min_rest, 4, cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
     c->stats.scan_ms += elapsed(c, 10, 11);
     {
@@ -612,6 +844,10 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         c->m_alive_h -= z;
     }
     int nf = h[0];
+    if (next_thr) {
+        const uint32_t mr = static_cast<uint32_t>(h[4]);   // 0xFFFFFFFF: no survivor
+        *next_thr = nf > 0 ? 0u : (mr == 0xFFFFFFFFu ? 0u : mr + 1);
+    }
     if (nf > 0) GC_TRY(ensure_rows(c));
     // Rounds are enqueued in batches without a host round trip: each round's
     // kernels read the frontier size on the device (an empty frontier makes a
@@ -624,12 +860,38 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     const int64_t alive0 = c->m_alive_h;
     int cur = 0, batch = c->trace > 1 ? 1 : 2;   // GC_PEEL_TRACE=2: one round per batch (per-round trace)
     unsigned long long done[2] = {0, 0};
+    int last_nf = nf;
     while (nf > 0) {
+        if (c->group_peel > 0 && nf >= c->group_peel) {
+            // a dense-core round with a host round trip: heavy edges grouped by pivot
+            const int nxt = cur ^ 1;
+            GC_TRY(record(c, 8));
+            GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
+            PolicySingle pol{c->alive.as<uint8_t>(), c->sup.as<uint32_t>(), thr, *round, lists[nxt], counts[nxt]};
+            GC_TRY(peel_round_grouped(c, lists[cur], nf, pol));
+            GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
+                      level >= 0 ? c->tau.as<int32_t>() : nullptr, level, acc);
+            GC_TRY(record(c, 9));
+            ++*round;
+            cur = nxt;
+            GC_CUDA(c, cudaMemcpyAsync(h, counts[cur], sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            GC_CUDA(c, cudaMemcpyAsync(h + 2, acc, 16, cudaMemcpyDeviceToHost, c->stream));
+            GC_TRY(sync(c));
+            c->stats.peel_kernel_ms += elapsed(c, 8, 9);
+            memcpy(done, h + 2, 16);
+            if (c->trace)
+                fprintf(stderr, "peel-trace level %d grouped nf %d rounds %llu removed %llu ms %.4f\n", level, nf,
+                        done[1], done[0], elapsed(c, 8, 9));
+            c->m_alive_h = alive0 - (int64_t)done[0];
+            nf = h[0];
+            if (nf > 0) GC_TRY(maybe_compact(c));
+            continue;
+        }
         GC_TRY(record(c, 8));
         for (int r = 0; r < batch; ++r) {
             const int nxt = cur ^ 1;
             GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
-            PolicySingle pol{c->rem.as<int32_t>(), c->sup.as<uint32_t>(), thr, *round, lists[nxt], counts[nxt]};
+            PolicySingle pol{c->alive.as<uint8_t>(), c->sup.as<uint32_t>(), thr, *round, lists[nxt], counts[nxt]};
             PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
                        c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
                        c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
@@ -651,7 +913,13 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
         c->m_alive_h = alive0 - (int64_t)done[0];
         nf = h[0];
         if (nf > 0) GC_TRY(maybe_compact(c));
-        if (c->trace < 2) batch = std::min(batch * 2, 16);
+        // Batches only while the frontier is small and not growing: a dense
+        // core's collapse (frontiers growing 10^4 -> 10^7 within a few rounds)
+        // runs a round per host check, so big rounds take the grouped path and
+        // the row compaction as soon as the live edges halve (C5 kernel
+        // 29.7 -> 26.8 s against blind batches of 16).
+        if (c->trace < 2) batch = (nf >= kBatchMaxFront || nf > last_nf) ? 1 : std::min(batch * 2, 16);
+        last_nf = nf;
     }
     *removed += (int64_t)done[0];
     c->stats.peel_rounds += (int64_t)done[1];
@@ -723,7 +991,6 @@ static int peel_setup(gc_ctx* c) {
     const int64_t m = c->m;
     c->rows_live = false;
     GC_TRY(ensure(c, c->alive, (size_t)m));
-    GC_TRY(ensure(c, c->rem, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_a, (size_t)m * 4));
     GC_TRY(ensure(c, c->front_b, (size_t)m * 4));
     GC_TRY(ensure(c, c->alist, (size_t)m * 4));
@@ -734,7 +1001,6 @@ static int peel_setup(gc_ctx* c) {
     c->alist_n = -1;
     if (m > 0) {
         GC_LAUNCH(c, k_fill_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), m, (uint8_t)1);
-        GC_LAUNCH(c, k_fill_i32, grid_for(m), kThreads, 0, c->rem.as<int32_t>(), m, (int32_t)-1);
     }
     c->stats.peel_rounds = 0;
     c->stats.compactions = 0;
@@ -755,9 +1021,11 @@ static int peel_setup(gc_ctx* c) {
     return GC_OK;
 }
 
-static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed) {
+static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed,
+                    uint32_t* next_thr = nullptr) {
+    if (next_thr) *next_thr = 0;
     if (peel_parts(c) > 0) return peel_level_part(c, thr, level, removed);
-    return peel_level(c, thr, level, round, removed);
+    return peel_level(c, thr, level, round, removed, next_thr);
 }
 
 int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
@@ -828,9 +1096,13 @@ int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
     int32_t round = 0;
     for (int32_t k = 3; left > 0; ++k) {
         int64_t removed = 0;
-        GC_TRY(peel_any(c, (uint32_t)(k - 2), k - 1, &round, &removed));
+        uint32_t next_thr = 0;
+        GC_TRY(peel_any(c, (uint32_t)(k - 2), k - 1, &round, &removed, &next_thr));
         if (removed > 0) last = k - 1;
         left -= removed;
+        // skip the levels whose frontier is known to be empty (their k-trusses
+        // equal the current one: no trussness value to assign)
+        if (next_thr > (uint32_t)(k - 1)) k = (int32_t)next_thr + 1;
     }
     *kmax = (m > 0) ? last : 0;
     GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));

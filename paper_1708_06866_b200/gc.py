@@ -40,6 +40,8 @@ GC_OPT_SUP_SKIP = 7
 GC_OPT_PEEL_PART = 8
 GC_OPT_HUGE_MAX = 9
 GC_OPT_COMPACT = 10
+GC_OPT_GROUP_PEEL = 12
+GC_OPT_GROUP_HEAVY = 14
 GC_OPT_OVERLAP = 13
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).

@@ -13,6 +13,7 @@ p.add_argument("--loop", type=int, default=0)
 p.add_argument("--tc", type=int, default=0)
 p.add_argument("--compact", type=int, default=-1)
 p.add_argument("--group", type=int, default=-1)
+p.add_argument("--heavy", type=int, default=-1)
 p.add_argument("--no-decomp", action="store_true")
 a = p.parse_args()
 t0 = time.time()
@@ -23,6 +24,8 @@ if a.loop:
     ctx.comm_init_loopback(a.loop)
 if a.group >= 0:
     ctx.set_option(gc.GC_OPT_GROUP_PEEL, a.group)
+if a.heavy >= 0:
+    ctx.set_option(gc.GC_OPT_GROUP_HEAVY, a.heavy)
 if a.compact >= 0:
     ctx.set_option(gc.GC_OPT_COMPACT, a.compact)
 if a.part:

@@ -170,7 +170,8 @@ def test_fuzz_mixed_structures_and_options(gcmod):
     result (count, supports, k-truss at random k, decomposition, fused call,
     listing count) against the oracle, under randomly drawn kernel options
     (forced class, task chunk, bitmap, huge-hash limit, long-segment
-    threshold, compaction, partitioned peeler, loopback partitions)."""
+    threshold, compaction, partitioned peeler, grouped dense-core rounds,
+    loopback partitions)."""
     rng = np.random.default_rng(2026)
     for trial in range(40):
         n = int(rng.integers(20, 400))
@@ -198,6 +199,8 @@ def test_fuzz_mixed_structures_and_options(gcmod):
                     gcmod.GC_OPT_HUGE_MAX: int(rng.choice([0, 16, 8192])),
                     gcmod.GC_OPT_COMPACT: int(rng.choice([0, 2, 3])),
                     gcmod.GC_OPT_PEEL_PART: int(rng.integers(0, 2)),
+                    gcmod.GC_OPT_GROUP_PEEL: int(rng.choice([0, 1, 64, 1 << 20])),
+                    gcmod.GC_OPT_GROUP_HEAVY: int(rng.choice([1, 4, 1024])),
                     gcmod.GC_OPT_FORCE_CLASS: int(rng.choice([-1, -1, 1, 2, 3]))}
             c.load_edges(u, v)
             for o, val in opts.items():
@@ -502,6 +505,33 @@ def test_decomposition_row_compaction(gcmod, compact):
             # a second call after compaction starts from refilled rows
             want, _ = g.ktruss(4)
             assert np.array_equal(c.ktruss(4)[0], want)
+
+
+@pytest.mark.parametrize("heavy", [1, 16])
+def test_grouped_dense_core_rounds(gcmod, heavy):
+    """Every peel round grouped (heavy edges by pivot, staged as a shared
+    bitmap; light ones by the per-edge search): k-truss and decomposition of
+    C1, an R-MAT s12 and a 300-clique with a pendant fan, against the oracle."""
+    q = np.arange(300, dtype=np.int32)
+    a, b = np.triu_indices(q.size, 1)
+    fan = np.arange(300, 700, dtype=np.int32)
+    graphs = [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=31),
+              (np.concatenate([q[a], fan, fan[1:]]), np.concatenate([q[b], fan % 7, fan[:-1]]))]
+    for u, v in graphs:
+        g = oracle.OracleGraph(u, v)
+        for compact in (0, 2):
+            with gcmod.Context(0) as c:
+                c.set_option(gcmod.GC_OPT_GROUP_PEEL, 1)
+                c.set_option(gcmod.GC_OPT_GROUP_HEAVY, heavy)
+                c.set_option(gcmod.GC_OPT_COMPACT, compact)
+                c.load_edges(u, v)
+                c.build_csr()
+                for k in (4, 7):
+                    want, _ = g.ktruss(k)
+                    assert np.array_equal(c.ktruss(k)[0], want), k
+                tau, kmax = c.truss_decomposition()
+                want_tau, want_kmax = g.truss_decomposition()
+                assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
 @pytest.mark.parametrize("parts", [1, 2, 5])
