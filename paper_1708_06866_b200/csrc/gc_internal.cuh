@@ -185,6 +185,7 @@ int triangle_count(gc_ctx* c, uint64_t* out);
 int support_dag(gc_ctx* c);   // fills c->sup (DAG order), all ranks combined
 unsigned long long* support_hits(gc_ctx* c);   // this rank's triangle count of the last support pass
 int scatter_canonical_u32(gc_ctx* c, const uint32_t* dag_vals, uint32_t* canon_out_dev);
+int scatter_canonical_u8(gc_ctx* c, const uint8_t* dag_vals, uint8_t* canon_out_dev);
 // peel.cu
 int build_sym(gc_ctx* c);
 int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive);

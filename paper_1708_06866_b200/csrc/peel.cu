@@ -641,17 +641,6 @@ __global__ void k_mask_from_support(const uint32_t* __restrict__ sup_canon, int6
         out[i] = sup_canon[i] != 0u;
 }
 
-__global__ void k_scatter_u8(const uint8_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
-                             uint8_t* __restrict__ out) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
-        out[eid[p]] = vals[p];
-}
-
-__global__ void k_scatter_i32(const int32_t* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
-                              int32_t* __restrict__ out) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x)
-        out[eid[p]] = vals[p];
-}
 
 }  // namespace
 
@@ -1063,8 +1052,7 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
                 GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->out_tmp.as<uint32_t>(), m,
                           c->out_tmp2.as<uint8_t>());
             } else {
-                GC_LAUNCH(c, k_scatter_u8, grid_for(m), kThreads, 0, c->alive.as<uint8_t>(), c->dag_eid.as<int32_t>(),
-                          m, c->out_tmp2.as<uint8_t>());
+                GC_TRY(scatter_canonical_u8(c, c->alive.as<uint8_t>(), c->out_tmp2.as<uint8_t>()));
             }
             GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
         }
@@ -1107,8 +1095,7 @@ int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
     *kmax = (m > 0) ? last : 0;
     GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
     if (m > 0)
-        GC_LAUNCH(c, k_scatter_i32, grid_for(m), kThreads, 0, c->tau.as<int32_t>(), c->dag_eid.as<int32_t>(), m,
-                  c->out_tmp.as<int32_t>());
+        GC_TRY(scatter_canonical_u32(c, c->tau.as<uint32_t>(), c->out_tmp.as<uint32_t>()));   // tau >= 2
     GC_TRY(record(c, 1));
     GC_TRY(copy_out(c, tau_out, c->out_tmp.p, (size_t)m * 4));
     GC_TRY(sync(c));

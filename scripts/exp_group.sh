@@ -1,4 +1,4 @@
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "grouped or fuzz or golden or c3 or compaction or c1 or c5 or king or partition" 2>&1 | tail -3
-for cfg in C3 C4 C5; do
-  timeout 300 python scripts/run_decomp.py --config $cfg 2>&1 | grep -E "decomposition"
-done
+python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "c3 or c4 or fuzz or golden or rmat or c1 or analysis" 2>&1 | tail -3
+python scripts/run_tc.py --config C4 --reps 3 --what analysis
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/run_tc.py --config C4 --reps 1 --what analysis > /dev/null 2>&1
+python bench.py --steps 5 --warmup 3 --no-extra --no-cpu-baseline > gpurun_out/bench_tmp.log 2>&1
