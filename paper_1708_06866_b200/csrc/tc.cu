@@ -371,6 +371,10 @@ struct SmemHash {
     __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
 
+#ifndef GC_DYN_BATCH
+#define GC_DYN_BATCH 1   // block classes fetch batches from a global counter (0: static round-robin)
+#endif
+
 struct KArgs {
     const int32_t* in_pos;
     const int32_t* in_src;
@@ -389,6 +393,7 @@ struct KArgs {
     int batch;                  // heavy-head kernel: consecutive tasks per batch
     int uw;                     // diagnostics: support roles skipped (GC_OPT_SUP_SKIP mask)
     int huge_max;               // class 3: largest d+ held in the shared hash
+    unsigned long long* next;   // block classes: batch counter (zeroed per launch; null: static dealing)
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -605,6 +610,8 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     // synchronises only when the head changes.  Invariant: the bitmap region
     // is all zero between heads.
     const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
+    __shared__ long long s_bt[2];
+    if (threadIdx.x == 0) s_bt[0] = blockIdx.x;
     for (int j = threadIdx.x; j < kZero; j += blockDim.x) bits[j] = 0u;
     int cur = -1, d = 0, lg = 0, ts = 0;
     int64_t r0 = 0;
@@ -632,7 +639,17 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
             }
         }
     };
-    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x)
+    __syncthreads();
+    // Batches after the first come from a global counter, in order: blocks
+    // stay on neighbouring heads (a static stride lets them drift apart) and
+    // no block is left with a long queue at the end.  The next batch id is
+    // fetched at the start of a batch into the other slot of s_bt; the
+    // barrier closing each batch publishes it.
+    for (int par = 0;; par ^= 1) {
+    const int64_t bt = s_bt[par];
+    if (bt >= nbatch) break;
+    if (threadIdx.x == 0)
+        s_bt[par ^ 1] = a.next ? (long long)gridDim.x + (long long)atomicAdd(a.next, 1ull) : bt + gridDim.x;
     for (int64_t t = bt * a.batch; t < min(a.ntask, (bt + 1) * a.batch); ++t) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
@@ -700,6 +717,7 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
         }
     }
     __syncthreads();
+    }
     if (cur >= 0) teardown(false);
     add_count(a.count, hits, lane);
 }
@@ -859,7 +877,10 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         return g;
     };
     // classes 3 and 2 first (heaviest tasks), then 1, 0
+    unsigned long long* next = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 640);   // classes 3, 2
+    if (GC_DYN_BATCH) GC_CUDA(c, cudaMemsetAsync(next, 0, 16, c->stream));
     if (c->ntask[3] > 0) {
+        a.next = GC_DYN_BATCH ? next : nullptr;
         a.tasks = tasks + c->task_off[3];
         a.ntask = c->ntask[3];
         const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
@@ -869,6 +890,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
     }
     if (c->ntask[2] > 0) {
+        a.next = GC_DYN_BATCH ? next + 1 : nullptr;
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
