@@ -131,6 +131,7 @@ struct gc_ctx {
     gcx::Buf live_len;  // int32[n] live entries at the front of each symmetric row
     gcx::Buf long_rows; // int32 rows longer than kLongRow (compacted block-wide)
     int nlong = 0;
+    gcx::Buf batch_slot;   // int64 per-block next-batch slots of the block-class kernels
     gcx::Buf grp_keys, grp_vals, grp_starts, grp_flags, grp_light;   // grouped dense-core rounds
     int group_peel = 1 << 20;   // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
     int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped

@@ -636,9 +636,17 @@ __global__ void k_finish_round_dev(const int32_t* __restrict__ front, const int*
 
 // mask from the canonical supports when the peel ran no round: it then only
 // removed zero-support edges (at the level scan), so alive = (S >= 1)
-__global__ void k_mask_from_support(const uint32_t* __restrict__ sup_canon, int64_t m, uint8_t* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = sup_canon[i] != 0u;
+// mask[i] = S[i] >= thr, and the number of kept edges (any order of S)
+__global__ void k_mask_from_support(const uint32_t* __restrict__ S, int64_t m, uint32_t thr,
+                                    uint8_t* __restrict__ out, unsigned long long* __restrict__ kept) {
+    unsigned c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const bool in = S[i] >= thr;
+        out[i] = in;
+        c += in;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(kept, (unsigned long long)c);
 }
 
 
@@ -1038,7 +1046,32 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
     }
     GC_TRY(record(c, 2));
     int64_t removed = 0;
-    if (alive_out || m_alive || c->nccl) {   // the peel is collective under a communicator
+    if (k <= 3) {
+        // The 2- and 3-trusses need no peel: an edge in no triangle (S = 0)
+        // changes no other support when it goes, so the k-truss is
+        // {e : S(e) >= k - 2} straight from the support pass (same on every
+        // rank: no collective).
+        c->stats.peel_rounds = 0;
+        if ((alive_out || m_alive) && m > 0) {
+            GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
+            GC_TRY(ensure(c, c->alive, (size_t)m));
+            unsigned long long* kept = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 656);
+            GC_CUDA(c, cudaMemsetAsync(kept, 0, 8, c->stream));
+            if (support_out) {           // canonical supports at hand: a coalesced pass
+                GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->out_tmp.as<uint32_t>(), m,
+                          (uint32_t)(k - 2), c->out_tmp2.as<uint8_t>(), kept);
+            } else {
+                GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->sup.as<uint32_t>(), m,
+                          (uint32_t)(k - 2), c->alive.as<uint8_t>(), kept);
+                GC_TRY(scatter_canonical_u8(c, c->alive.as<uint8_t>(), c->out_tmp2.as<uint8_t>()));
+            }
+            if (alive_out) GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
+            GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 520, kept, 8, cudaMemcpyDeviceToHost,
+                                       c->stream));
+            GC_TRY(sync(c));
+            removed = m - (int64_t)*reinterpret_cast<uint64_t*>(static_cast<char*>(c->hpin) + 520);
+        }
+    } else if (alive_out || m_alive || c->nccl) {   // the peel is collective under a communicator
         GC_TRY(peel_setup(c));
         if (m > 0 && k > 2) {
             int32_t round = 0;
@@ -1046,11 +1079,12 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
         }
         if (alive_out && m > 0) {
             GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
-            if (support_out && c->stats.peel_rounds == 0 && k > 2) {
+            if (support_out && c->stats.peel_rounds == 0) {
                 // no round ran: only zero-support edges left, read the mask off the
                 // canonical supports (coalesced) instead of scattering the DAG-order one
-                GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->out_tmp.as<uint32_t>(), m,
-                          c->out_tmp2.as<uint8_t>());
+                unsigned long long* kept = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 656);
+                GC_LAUNCH(c, k_mask_from_support, grid_for(m), kThreads, 0, c->out_tmp.as<uint32_t>(), m, 1u,
+                          c->out_tmp2.as<uint8_t>(), kept);
             } else {
                 GC_TRY(scatter_canonical_u8(c, c->alive.as<uint8_t>(), c->out_tmp2.as<uint8_t>()));
             }

@@ -394,6 +394,7 @@ struct KArgs {
     int uw;                     // diagnostics: support roles skipped (GC_OPT_SUP_SKIP mask)
     int huge_max;               // class 3: largest d+ held in the shared hash
     unsigned long long* next;   // block classes: batch counter (zeroed per launch; null: static dealing)
+    long long* slot;            // ... and 2 slots per block publishing the next batch id to its warps
 };
 
 __device__ __forceinline__ bool owned(const KArgs& a, int i0) {
@@ -610,7 +611,10 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     // synchronises only when the head changes.  Invariant: the bitmap region
     // is all zero between heads.
     const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
-    __shared__ long long s_bt[2];
+    // the next batch id goes through global memory (a per-block slot pair):
+    // 16 more bytes of static shared memory would cost the support kernel a
+    // resident block per SM (4 x 57,344 B + reserve fill the SM exactly)
+    long long* s_bt = a.slot + 2 * blockIdx.x;
     if (threadIdx.x == 0) s_bt[0] = blockIdx.x;
     for (int j = threadIdx.x; j < kZero; j += blockDim.x) bits[j] = 0u;
     int cur = -1, d = 0, lg = 0, ts = 0;
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     // fetched at the start of a batch into the other slot of s_bt; the
     // barrier closing each batch publishes it.
     for (int par = 0;; par ^= 1) {
-    const int64_t bt = s_bt[par];
+    const int64_t bt = *(volatile long long*)(s_bt + par);
     if (bt >= nbatch) break;
     if (threadIdx.x == 0)
         s_bt[par ^ 1] = a.next ? (long long)gridDim.x + (long long)atomicAdd(a.next, 1ull) : bt + gridDim.x;
@@ -879,25 +883,29 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     // classes 3 and 2 first (heaviest tasks), then 1, 0
     unsigned long long* next = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 640);   // classes 3, 2
     if (GC_DYN_BATCH) GC_CUDA(c, cudaMemsetAsync(next, 0, 16, c->stream));
+    GC_TRY(ensure(c, c->batch_slot, 2 * 2 * 4096 * sizeof(long long)));   // classes 3 and 2, grid <= 4096
+    long long* slots = c->batch_slot.as<long long>();
     if (c->ntask[3] > 0) {
         a.next = GC_DYN_BATCH ? next : nullptr;
+        a.slot = slots;
         a.tasks = tasks + c->task_off[3];
         a.ntask = c->ntask[3];
         const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
         constexpr int threads = 32 * GC_HUGE_WARPS(SUP);
         const int grid = prep(3, k_tc_block<SUP, true>, smem, threads);
         if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block huge)", __FILE__, __LINE__);
-        GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
+        GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
     }
     if (c->ntask[2] > 0) {
         a.next = GC_DYN_BATCH ? next + 1 : nullptr;
+        a.slot = slots + 2 * 4096;
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
         const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
         constexpr int threads = 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS);
         const int grid = prep(2, k_tc_block<SUP, false>, smem, threads);
         if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block)", __FILE__, __LINE__);
-        GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>(grid, a.ntask), threads, smem, a);
+        GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
     }
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
