@@ -859,7 +859,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     unsigned long long done[2] = {0, 0};
     int last_nf = nf;
     while (nf > 0) {
-        if (c->group_peel > 0 && nf >= c->group_peel) {
+        if (c->group_peel > 0 && nf >= c->group_peel && c->stats.max_degree >= c->group_heavy) {
             // a dense-core round with a host round trip: heavy edges grouped by pivot
             const int nxt = cur ^ 1;
             GC_TRY(record(c, 8));
