@@ -371,27 +371,45 @@ def main():
         hs = torch.empty(m, dtype=torch.int32).pin_memory()
         hm = torch.empty(m, dtype=torch.uint8).pin_memory()
 
-        def e2e_step():
-            ctx.load_edges(hu, hv)
-            ctx.build_csr()
-            ctx.ktruss_analysis(k, hs, hm)
+        def e2e_run(steps, pipelined):
+            # Every step copies its raw list host -> device and reads its supports
+            # and mask back.  Pipelined: step i+1's copy (gc_stage_edges, a library
+            # copy stream) runs while step i's support pass computes, so the
+            # K copies of K steps all fall inside the timed region.
+            if pipelined:
+                ctx.stage_edges(hu, hv)
+            for i in range(steps):
+                if pipelined:
+                    ctx.build_csr()                     # waits for this step's staged copy
+                    if i + 1 < steps:
+                        ctx.stage_edges(hu, hv)         # the next step's input
+                else:
+                    ctx.load_edges(hu, hv)
+                    ctx.build_csr()
+                ctx.ktruss_analysis(k, hs, hm)
 
-        e2e_step()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        barrier()
-        te = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
-        e2e = {"value": m / (te / args.steps / 1e3), "unit": "edges/s", "h2d_bytes_per_step": 2 * nnz * 4,
-               "d2h_bytes_per_step": m * 4 + m * 1 + 8}
+        def e2e_time(pipelined):
+            e2e_run(1, pipelined)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_run(args.steps, pipelined)
+            e1.record(stream)
+            barrier()
+            te = e0.elapsed_time(e1)
+            if world > 1:
+                tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te = float(tt.item())
+            return m / (te / args.steps / 1e3)
+
+        serial = e2e_time(False)
+        e2e = {"value": e2e_time(True), "unit": "edges/s", "h2d_bytes_per_step": 2 * nnz * 4,
+               "d2h_bytes_per_step": m * 4 + m * 1 + 8,
+               "api": "gc_stage_edges (pinned host u, v) + gc_build_csr + gc_ktruss_analysis(k) into pinned host "
+                      "supports and mask; step i+1's host->device copy overlaps step i's kernels",
+               "serial_value": serial}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

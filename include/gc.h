@@ -110,6 +110,20 @@ int gc_comm_init_loopback(gc_ctx* ctx, int nparts);
  * reported by gc_build_csr. */
 int gc_load_edges(gc_ctx* ctx, const int32_t* u, const int32_t* v, int64_t nnz);
 
+/* gc_stage_edges: the load step (a1) of the NEXT graph, overlapped with work
+ * on the current one.  Enqueues the copy of u, v (same meaning and checks
+ * as gc_load_edges) on a library copy stream and returns at once; the
+ * current edge list, CSR and results stay valid and usable.  The next
+ * gc_build_csr waits for the copy and builds from the staged list.  A second
+ * gc_stage_edges first waits for the pending copy and then replaces it;
+ * gc_load_edges waits for and discards it.
+ * Ownership: the caller keeps u, v and must leave them unchanged until that
+ * gc_build_csr returns.  Page-locked host memory (or device memory) gives a
+ * copy that overlaps the kernels; pageable host memory is accepted but the
+ * driver copies it before returning.  Errors: as gc_load_edges; copy
+ * failures are reported here or by the gc_build_csr that consumes it. */
+int gc_stage_edges(gc_ctx* ctx, const int32_t* u, const int32_t* v, int64_t nnz);
+
 /* gc_build_csr (north star): on the GPU, drop self loops, fold both
  * orientations and duplicates, sort into the canonical list;
  * compute degrees ("d = sum(E)"); rank vertices by (degree, id) and

@@ -3,6 +3,8 @@
 #include <cstring>
 #include <new>
 
+#include <utility>
+
 #include "gc_internal.cuh"
 
 namespace gcx {
@@ -174,8 +176,9 @@ int gc_create(gc_ctx** out, int device, void* cuda_stream) {
 int gc_destroy(gc_ctx* c) {
     if (!c) return GC_OK;
     cudaSetDevice(c->device);
+    if (c->copy_s) cudaStreamSynchronize(c->copy_s);
     cudaStreamSynchronize(c->stream);
-    gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
+    gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->stage_u, &c->stage_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
                         &c->dag_col, &c->dag_src, &c->dag_eid, &c->in_ptr, &c->in_pos, &c->in_src,
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
@@ -188,6 +191,8 @@ int gc_destroy(gc_ctx* c) {
     for (auto& ev : c->ev)
         if (ev) cudaEventDestroy(ev);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->copy_s) cudaStreamDestroy(c->copy_s);
+    if (c->ev_staged) cudaEventDestroy(c->ev_staged);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -248,10 +253,42 @@ int gc_comm_init_loopback(gc_ctx* c, int nparts) {
     return GC_OK;
 }
 
+// wait for a pending gc_stage_edges copy (it may still read the caller's buffers)
+static int drain_stage(gc_ctx* c) {
+    if (c->copy_s) GC_CUDA(c, cudaStreamSynchronize(c->copy_s));
+    return GC_OK;
+}
+
+int gc_stage_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
+    GC_TRY(check_ctx(c));
+    if (nnz < 0 || (nnz > 0 && (!u || !v))) return fail(c, GC_ERR_INVALID, "gc_stage_edges: bad arguments");
+    cudaSetDevice(c->device);
+    if (!c->copy_s) {
+        GC_CUDA(c, cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking));
+        GC_CUDA(c, cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming));
+    }
+    GC_TRY(drain_stage(c));
+    c->stage_nnz = -1;
+    GC_TRY(ensure(c, c->stage_u, (size_t)nnz * sizeof(int32_t)));   // allocation is ordered on the context stream
+    GC_TRY(ensure(c, c->stage_v, (size_t)nnz * sizeof(int32_t)));
+    GC_CUDA(c, cudaEventRecord(c->ev_staged, c->stream));            // buffers ready before the copy
+    GC_CUDA(c, cudaStreamWaitEvent(c->copy_s, c->ev_staged, 0));
+    if (nnz > 0) {
+        GC_CUDA(c, cudaMemcpyAsync(c->stage_u.p, u, (size_t)nnz * 4, cudaMemcpyDefault, c->copy_s));
+        GC_CUDA(c, cudaMemcpyAsync(c->stage_v.p, v, (size_t)nnz * 4, cudaMemcpyDefault, c->copy_s));
+    }
+    GC_CUDA(c, cudaEventRecord(c->ev_staged, c->copy_s));
+    c->stage_nnz = nnz;
+    if (c->state < 1) c->state = 1;   // gc_build_csr may follow directly
+    return GC_OK;
+}
+
 int gc_load_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
     GC_TRY(check_ctx(c));
     if (nnz < 0 || (nnz > 0 && (!u || !v))) return fail(c, GC_ERR_INVALID, "gc_load_edges: bad arguments");
     cudaSetDevice(c->device);
+    GC_TRY(drain_stage(c));
+    c->stage_nnz = -1;
     GC_TRY(ensure(c, c->raw_u, (size_t)nnz * sizeof(int32_t)));
     GC_TRY(ensure(c, c->raw_v, (size_t)nnz * sizeof(int32_t)));
     GC_TRY(copy_in(c, c->raw_u.p, u, (size_t)nnz * sizeof(int32_t)));
@@ -269,9 +306,19 @@ int gc_build_csr(gc_ctx* c) {
     GC_TRY(check_ctx(c));
     if (c->state < 1) return fail(c, GC_ERR_STATE, "gc_build_csr before gc_load_edges");
     cudaSetDevice(c->device);
+    if (c->stage_nnz >= 0) {
+        // a staged list: the context stream waits for its copy, then the
+        // staged and current raw buffers trade places
+        GC_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_staged, 0));
+        std::swap(c->raw_u, c->stage_u);
+        std::swap(c->raw_v, c->stage_v);
+        c->nnz = c->stage_nnz;
+        c->stage_nnz = -1;
+    }
     c->state = 1;
     c->tasks_ready = false;
     c->sym_ready = false;
+    c->n = c->m = 0;
     GC_TRY(record(c, 0));
     GC_TRY(build_csr(c));
     GC_TRY(prepare_tasks(c));

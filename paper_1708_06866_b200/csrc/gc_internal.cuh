@@ -78,6 +78,10 @@ struct gc_ctx {
 
     // raw input (a1)
     gcx::Buf raw_u, raw_v;
+    gcx::Buf stage_u, stage_v;       // gc_stage_edges: the next graph's raw list
+    int64_t stage_nnz = -1;          // >= 0: a staged list waits for the next gc_build_csr
+    cudaStream_t copy_s = nullptr;   // library-owned copy stream of gc_stage_edges (lazy)
+    cudaEvent_t ev_staged = nullptr;
     int64_t nnz = 0;
 
     // graph sizes

@@ -47,7 +47,7 @@ GC_OPT_OVERLAP = 13
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "gc_create", "gc_destroy", "gc_last_error", "gc_nccl_unique_id", "gc_comm_init",
-    "gc_comm_init_loopback", "gc_load_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
+    "gc_comm_init_loopback", "gc_load_edges", "gc_stage_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
     "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_ktruss_analysis",
     "gc_truss_decomposition", "gc_list_triangles",
     "gc_set_option", "gc_get_stats", "gc_reset_stats", "gc_partition_bounds",
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "gc_comm_init": ([_vp, _vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "gc_comm_init_loopback": ([_vp, ctypes.c_int], ctypes.c_int),
         "gc_load_edges": ([_vp, _vp, _vp, _i64], ctypes.c_int),
+        "gc_stage_edges": ([_vp, _vp, _vp, _i64], ctypes.c_int),
         "gc_build_csr": ([_vp], ctypes.c_int),
         "gc_num_vertices": ([_vp, ctypes.POINTER(_i64)], ctypes.c_int),
         "gc_num_edges": ([_vp, ctypes.POINTER(_i64)], ctypes.c_int),
@@ -172,6 +173,7 @@ class Context:
         if rc != GC_OK:
             raise GcError(rc, self._L.gc_last_error(None).decode())
         self._h = h
+        self._staged = None
         self.device = device
         self._keep = []
 
@@ -213,8 +215,22 @@ class Context:
             raise ValueError("u and v differ in length")
         self._check(self._L.gc_load_edges(self._h, _vp(_ptr(u)), _vp(_ptr(v)), n))
 
+    def stage_edges(self, u, v):
+        """gc_stage_edges: start copying the next graph's raw list while the
+        current one is in use; the next build_csr consumes it.  The arrays are
+        kept referenced until then (page-locked host or device memory overlaps
+        the copy with the kernels)."""
+        u = _as_i32(u)
+        v = _as_i32(v)
+        n = int(u.shape[0])
+        if int(v.shape[0]) != n:
+            raise ValueError("u and v differ in length")
+        self._check(self._L.gc_stage_edges(self._h, _vp(_ptr(u)), _vp(_ptr(v)), n))
+        self._staged = (u, v)
+
     def build_csr(self):
         self._check(self._L.gc_build_csr(self._h))
+        self._staged = None
 
     def num_vertices(self) -> int:
         x = _i64()

@@ -1,5 +1,2 @@
-for lib in build_var/old/libgc.so paper_1708_06866_b200/libgc.so build_var/static/libgc.so; do
-echo $lib
-GC_LIB_PATH=$lib python scripts/run_tc.py --config C4 --reps 3 --what analysis | cut -c1-120
-GC_LIB_PATH=$lib python scripts/run_tc.py --config C5 --reps 2 --what tc,support | cut -c1-120
-done
+python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "staged or golden or errors or device" 2>&1 | tail -2
+python bench.py --steps 5 --warmup 3 --no-extra --no-cpu-baseline > gpurun_out/bench_tmp.log 2>&1; echo rc=$?

@@ -632,6 +632,44 @@ def test_ktruss_analysis_one_pass(gcmod, parts):
 
 
 # --------------------------------------------------- API / pointer kinds ----
+def test_staged_edges(gcmod):
+    """gc_stage_edges: the next graph's copy is enqueued while the current one
+    stays usable; the next build consumes it.  Host (pageable and pinned) and
+    device sources, staging as the first call, a replaced stage, and a stage
+    discarded by gc_load_edges, all against the oracle."""
+    import torch
+    ga = gen.rmat(11, 16, seed=41)
+    gb = gen.rmat(12, 8, seed=42)
+    gcx = gen.rmat(10, 16, seed=43)
+    oa, ob, oc = (oracle.OracleGraph(*g) for g in (ga, gb, gcx))
+    with gcmod.Context(0) as c:
+        c.stage_edges(*ga)                                    # first call: stage, then build
+        c.build_csr()
+        assert c.triangle_count() == oa.triangle_count()
+        pu = torch.from_numpy(gb[0]).pin_memory()
+        pv = torch.from_numpy(gb[1]).pin_memory()
+        c.stage_edges(pu, pv)                                 # graph A stays valid meanwhile
+        assert np.array_equal(c.edge_support(), oa.support())
+        cu, cv = c.get_edges()
+        assert np.array_equal(cu, oa.cu) and np.array_equal(cv, oa.cv)
+        c.build_csr()
+        assert c.triangle_count() == ob.triangle_count()
+        assert np.array_equal(c.edge_support(), ob.support())
+        c.stage_edges(*ga)                                    # replaced before use
+        c.stage_edges(torch.from_numpy(gcx[0]).cuda(), torch.from_numpy(gcx[1]).cuda())
+        c.build_csr()
+        assert np.array_equal(c.edge_support(), oc.support())
+        want, _ = oc.ktruss(4)
+        assert np.array_equal(c.ktruss(4)[0], want)
+        c.stage_edges(*gb)                                    # discarded by gc_load_edges
+        c.load_edges(*ga)
+        c.build_csr()
+        assert c.triangle_count() == oa.triangle_count()
+        c.stage_edges(np.zeros(0, np.int32), np.zeros(0, np.int32))   # empty graph
+        c.build_csr()
+        assert c.num_edges() == 0 and c.triangle_count() == 0
+
+
 def test_device_pointers_and_determinism(ctx):
     import torch
     u, v = gen.rmat(12, 16, seed=21)
