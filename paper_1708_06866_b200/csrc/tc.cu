@@ -64,7 +64,10 @@ constexpr int kTS3 = 16384;    // huge-head hash slots (d+ <= kTS3/2 by default)
 constexpr int kD2H = 2048;     // largest d+ the heavy-head hash takes (load <= 1/2)
 constexpr int kWarps = 8;                   // 256 threads per block
 #ifndef GC_SUP_WARPS
-#define GC_SUP_WARPS 10                     // heavy-head support kernel: warps per block sharing one table
+#define GC_SUP_WARPS 16                     // heavy-head support kernel: warps per block sharing one table
+                                            // (4 x 16 = the SM's 64 warps at 32 registers, a 72-byte spill:
+                                            // C4 110.2 -> 102.0 ms against 10 warps at 48 registers; the
+                                            // kernel is latency-bound, so occupancy beats the spill)
 #endif
 #ifndef GC_SUP_MINB
 #define GC_SUP_MINB 4                       // ... and resident blocks per SM (register budget)
@@ -77,7 +80,8 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #endif
 #define GC_HUGE_WARPS(S) ((S) ? GC_HUGE_WARPS_SUP : GC_HUGE_WARPS_TC)
 #ifndef GC_TC_WARPS
-#define GC_TC_WARPS 10                      // heavy-head count kernel: warps per block
+#define GC_TC_WARPS 12                      // heavy-head count kernel: warps per block (5 x 12 = 60 warps
+                                            // at 32 registers: C4 51.0 -> 49.2 ms, C5 545 -> 523 ms)
 #endif
 #ifndef GC_TC_MINB
 #define GC_TC_MINB 5

@@ -1,2 +1,5 @@
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "staged or golden or errors or device" 2>&1 | tail -2
-python bench.py --steps 5 --warmup 3 --no-extra --no-cpu-baseline > gpurun_out/bench_tmp.log 2>&1; echo rc=$?
+for lib in paper_1708_06866_b200/libgc.so build_var/t12/libgc.so build_var/t16/libgc.so; do
+echo $lib
+GC_LIB_PATH=$lib python scripts/run_tc.py --config C4 --reps 3 --what tc,support | tail -1 | cut -c1-130
+GC_LIB_PATH=$lib python scripts/run_tc.py --config C5 --reps 2 --what tc,support | tail -1 | cut -c1-130
+done

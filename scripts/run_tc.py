@@ -12,11 +12,15 @@ p.add_argument("--config", default="C3")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--what", default="tc,support")
 p.add_argument("--chunk", type=int, default=0)
+p.add_argument("--opt", action="append", default=[], help="OPTION_ID=VALUE (gc_set_option)")
 a = p.parse_args()
 u, v = gen.CONFIGS[a.config].generate()
 ctx = Context(0, torch.cuda.current_stream())
 if a.chunk:
     ctx.set_option(2, a.chunk)
+for o in a.opt:
+    oid, oval = o.split("=")
+    ctx.set_option(int(oid), int(oval))
 ctx.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
 for r in range(a.reps):
     ctx.build_csr()
