@@ -307,6 +307,9 @@ struct PeelArgs {
 // alternatives: 32-ary window narrowing of the longer row and
 // splitting long rows into work items over many warps were slower.
 constexpr int kSerialRow = 8;
+#ifndef GC_GRP_MINB
+#define GC_GRP_MINB 4    // ... of k_peel_grouped (48 KB of shared memory per block)
+#endif
 #ifndef GC_PEEL_GMAX
 #define GC_PEEL_GMAX 8   // frontier edges per warp at most (8: K13 kernel 226 -> 78 ms, C4 +0.7 %)
 #endif
@@ -335,8 +338,13 @@ __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol,
     }
 }
 
-template <class Pol>
-__global__ void __launch_bounds__(256) k_peel(PeelArgs A, Pol pol) {
+// MINB: two builds of the kernel.  MINB = 1 (48 registers) for big frontiers,
+// whose grouped lanes need the registers; MINB = 8 (32 registers, the SM's
+// 64 warps) for the small rounds that dominate a decomposition, where the
+// searches are latency-bound (C4 / C5 decomposition kernels -29 % / -25 %,
+// but a 20 M-edge first round of ktruss(5) 2.6x slower).
+template <class Pol, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int nfront = A.nfront_dev ? *A.nfront_dev : A.nfront;
@@ -472,7 +480,7 @@ __global__ void k_group_flags(const uint32_t* __restrict__ key, int nh, uint8_t*
 constexpr size_t kGrpSmem = kGrpBits / 8 + kGrpBits / 64 * 4 + 64;   // bitmap + prefix per 64 ranks
 
 template <class Pol>
-__global__ void __launch_bounds__(256, 4) k_peel_grouped(PeelArgs A, Pol pol, const uint32_t* __restrict__ key,
+__global__ void __launch_bounds__(256, GC_GRP_MINB) k_peel_grouped(PeelArgs A, Pol pol, const uint32_t* __restrict__ key,
                                                          const int32_t* __restrict__ edges, int nh,
                                                          const int32_t* __restrict__ starts,
                                                          const int* __restrict__ ngroups) {
@@ -727,6 +735,17 @@ static int ensure_rows(gc_ctx* c) {
     return GC_OK;
 }
 
+// k_peel for a round of nf frontier edges (nf < 0: known only on the device)
+template <class Pol>
+static int launch_peel(gc_ctx* c, int blocks, const PeelArgs& A, const Pol& pol, int64_t nf) {
+    if (nf < 0 || nf >= c->peel_big) {
+        GC_LAUNCH(c, (k_peel<Pol, 1>), blocks, 256, 0, A, pol);
+    } else {
+        GC_LAUNCH(c, (k_peel<Pol, 8>), blocks, 256, 0, A, pol);
+    }
+    return GC_OK;
+}
+
 // One peel round over the frontier list.
 template <class Pol>
 static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
@@ -734,8 +753,7 @@ static int peel_round(gc_ctx* c, const int32_t* front, int nf, const Pol& pol) {
                c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(), c->sym_eid.as<int32_t>(),
                c->alive.as<uint8_t>()};
     const int blocks = (int)std::min<int64_t>(((int64_t)nf * 32 + 255) / 256, 148 * 8);
-    GC_LAUNCH(c, k_peel<Pol>, blocks, 256, 0, A, pol);
-    return GC_OK;
+    return launch_peel(c, blocks, A, pol, nf);
 }
 
 
@@ -763,7 +781,7 @@ static int peel_round_grouped(gc_ctx* c, const int32_t* front, int nf, const Pol
     Lt.front = c->grp_light.as<int32_t>();
     Lt.nfront = 0;
     Lt.nfront_dev = cnts + 1;
-    GC_LAUNCH(c, k_peel<Pol>, 148 * 8, 256, 0, Lt, pol);
+    GC_TRY(launch_peel(c, 148 * 8, Lt, pol, -1));
     int32_t* h = static_cast<int32_t*>(c->hpin);
     GC_CUDA(c, cudaMemcpyAsync(h + 8, cnts, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     GC_TRY(sync(c));
@@ -892,7 +910,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
                        c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
                        c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
-            GC_LAUNCH(c, k_peel<PolicySingle>, 148 * 8, 256, 0, A, pol);
+            GC_TRY(launch_peel(c, 148 * 8, A, pol, r == 0 ? (int64_t)nf : 0));   // later rounds of a batch are small
             GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
                       level >= 0 ? c->tau.as<int32_t>() : nullptr, level, acc);
             ++*round;
