@@ -83,6 +83,13 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #define GC_TC_WARPS 12                      // heavy-head count kernel: warps per block (5 x 12 = 60 warps
                                             // at 32 registers: C4 51.0 -> 49.2 ms, C5 545 -> 523 ms)
 #endif
+#ifndef GC_WARP_MINB
+#define GC_WARP_MINB 8                      // warp-task kernel (class 1): resident blocks per SM to budget for
+                                            // (8: 32 registers, 64 warps; C4 support -2 % next to the block kernel)
+#endif
+#ifndef GC_TINY_MINB
+#define GC_TINY_MINB 8                      // lane-task kernel (class 0)
+#endif
 #ifndef GC_TC_MINB
 #define GC_TC_MINB 5
 #endif
@@ -420,7 +427,7 @@ __device__ __forceinline__ void add_count(unsigned long long* count, uint32_t hi
 // warp thus keeps 32 independent tasks' loads in flight instead of
 // building a shared table per head.  Suffix scans stop past max N+(v).
 template <bool SUP>
-__global__ void __launch_bounds__(256) k_tc_tiny(KArgs a) {
+__global__ void __launch_bounds__(256, GC_TINY_MINB) k_tc_tiny(KArgs a) {
     const int lane = threadIdx.x & 31;
     uint32_t hits = 0;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(256) k_tc_tiny(KArgs a) {
 
 // ------------------------------------------------- warp-task kernel (1) --
 template <int TS, bool SUP>
-__global__ void __launch_bounds__(256) k_tc_warp(KArgs a) {
+__global__ void __launch_bounds__(256, GC_WARP_MINB) k_tc_warp(KArgs a) {
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int per_warp = SUP ? 3 * TS : TS;
