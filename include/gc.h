@@ -178,6 +178,22 @@ int gc_ktruss(gc_ctx* ctx, int32_t k, uint8_t* alive_out, int64_t* m_alive);
 int gc_ktruss_analysis(gc_ctx* ctx, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
                        int64_t* m_alive);
 
+/* gc_ktruss_analysis_async: gc_ktruss_analysis whose per-edge outputs
+ * (support_out, alive_out) are copied back on a library copy stream: the
+ * call returns once they are computed, with *triangles and *m_alive already
+ * valid, while the copies run (overlapping e.g. the next gc_stage_edges /
+ * gc_build_csr).  The two buffers may be read only after gc_wait returns
+ * (or after the next call on this context that produces per-edge outputs,
+ * which waits for them on the device before reusing its staging memory).
+ * Page-locked host buffers give the overlap; pageable ones are copied
+ * before return.  Arguments and errors as gc_ktruss_analysis. */
+int gc_ktruss_analysis_async(gc_ctx* ctx, int32_t k, uint64_t* triangles, uint32_t* support_out,
+                             uint8_t* alive_out, int64_t* m_alive);
+
+/* gc_wait: block until every asynchronous copy of this context
+ * (gc_ktruss_analysis_async outputs, a pending gc_stage_edges) is done. */
+int gc_wait(gc_ctx* ctx);
+
 /* gc_list_triangles (Alg. 1's triangle records; SURVEY §8(f)
  * NEXT #3): every triangle once as three ORIGINAL vertex ids, ascending
  * within the triple; triples in unspecified order.  tri_out: 3 * capacity

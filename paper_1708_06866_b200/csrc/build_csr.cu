@@ -308,7 +308,7 @@ int build_csr(gc_ctx* c) {
     if (nnz > 0)
         GC_LAUNCH(c, k_scan_ids, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
                   d_scal, d_scal + 1);
-    GC_CUDA(c, cudaMemcpyAsync(h, d_scal, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, d_scal, 2 * sizeof(int)));
     GC_TRY(sync(c));
     int maxid = reinterpret_cast<int*>(h)[0];
     int neg = reinterpret_cast<int*>(h)[1];
@@ -359,11 +359,11 @@ int build_csr(gc_ctx* c) {
         GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
                                              d_nsel, nnz, c->stream));
         c->stats.lib_launches += 2;
-        GC_CUDA(c, cudaMemcpyAsync(h, d_nsel, 8, cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(read_small(c, h, d_nsel, 8));
         GC_TRY(sync(c));
         int64_t nsel = h[0];
         if (nsel > 0) {
-            GC_CUDA(c, cudaMemcpyAsync(h + 1, c->canon.as<uint64_t>() + nsel - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+            GC_TRY(read_small(c, h + 1, c->canon.as<uint64_t>() + nsel - 1, 8));
             GC_TRY(sync(c));
             m = nsel - ((uint64_t)h[1] == sent ? 1 : 0);
         }
@@ -407,7 +407,7 @@ int build_csr(gc_ctx* c) {
         int* d_maxdeg = d_scal + 4;
         GC_CUDA(c, cudaMemsetAsync(d_maxdeg, 0, sizeof(int), c->stream));
         GC_LAUNCH(c, k_vkeys, grid_for(n), kThreads, 0, c->deg.as<int32_t>(), n, vk, ids, d_maxdeg);
-        GC_CUDA(c, cudaMemcpyAsync(h, d_maxdeg, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(read_small(c, h, d_maxdeg, sizeof(int)));
         GC_TRY(sync(c));
         const int dbits = std::max(1, ceil_log2_u64((uint64_t)reinterpret_cast<int*>(h)[0] + 1));
         size_t tmp = 0;
@@ -469,7 +469,7 @@ int build_csr(gc_ctx* c) {
     if (n > 0)
         GC_LAUNCH(c, k_graph_stats, grid_for(n), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(),
                   c->deg.as<int32_t>(), c->dag_col.as<int32_t>(), n, acc);
-    GC_CUDA(c, cudaMemcpyAsync(h, acc, 13 * 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, acc, 13 * 8));
     GC_TRY(sync(c));
     c->stats.n = n;
     c->stats.m = m;

@@ -65,7 +65,8 @@ int host_scratch(gc_ctx* c, size_t bytes) {
     if (c->hpin) cudaFreeHost(c->hpin);
     c->hpin = nullptr;
     c->hpin_cap = 0;
-    GC_CUDA(c, cudaMallocHost(&c->hpin, bytes));
+    GC_CUDA(c, cudaHostAlloc(&c->hpin, bytes, cudaHostAllocMapped));
+    GC_CUDA(c, cudaHostGetDevicePointer(&c->hpin_dev, c->hpin, 0));
     c->hpin_cap = bytes;
     return GC_OK;
 }
@@ -88,6 +89,51 @@ int copy_out(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes) {
     if (nbytes == 0) return GC_OK;
     cudaMemcpyKind kind = is_device_ptr(dst) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     GC_CUDA(c, cudaMemcpyAsync(dst, src_dev, nbytes, kind, c->stream));
+    return GC_OK;
+}
+
+__global__ void k_read_small(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+int read_small(gc_ctx* c, void* host_dst, const void* src_dev, size_t nbytes) {
+    // host_dst lies in the context's page-locked scratch, mapped into the
+    // device address space: one tiny kernel writes it, so the read needs no
+    // copy engine (whose FIFO may hold a long asynchronous read-back)
+    char* h = static_cast<char*>(host_dst);
+    char* base = static_cast<char*>(c->hpin);
+    if (!c->hpin_dev || h < base || h + nbytes > base + c->hpin_cap || nbytes > 4096) {
+        GC_CUDA(c, cudaMemcpyAsync(host_dst, src_dev, nbytes, cudaMemcpyDeviceToHost, c->stream));
+        return GC_OK;
+    }
+    k_read_small<<<1, 128, 0, c->stream>>>(static_cast<const uint8_t*>(src_dev),
+                                           reinterpret_cast<uint8_t*>(static_cast<char*>(c->hpin_dev) + (h - base)),
+                                           (int)nbytes);
+    GC_CUDA(c, cudaGetLastError());
+    ++c->stats.launches;
+    return GC_OK;
+}
+
+int copy_out_staged(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes) {
+    if (!c->async_out) return copy_out(c, dst, src_dev, nbytes);
+    if (nbytes == 0) return GC_OK;
+    if (!c->d2h_s) {
+        GC_CUDA(c, cudaStreamCreateWithFlags(&c->d2h_s, cudaStreamNonBlocking));
+        GC_CUDA(c, cudaEventCreateWithFlags(&c->ev_out_ready, cudaEventDisableTiming));
+        GC_CUDA(c, cudaEventCreateWithFlags(&c->ev_d2h_done, cudaEventDisableTiming));
+    }
+    GC_CUDA(c, cudaEventRecord(c->ev_out_ready, c->stream));
+    GC_CUDA(c, cudaStreamWaitEvent(c->d2h_s, c->ev_out_ready, 0));
+    // a copy engine: the context stream's own small reads (read_small) do
+    // not queue behind it, and the SMs stay free for the next call's kernels
+    GC_CUDA(c, cudaMemcpyAsync(dst, src_dev, nbytes, cudaMemcpyDefault, c->d2h_s));
+    GC_CUDA(c, cudaEventRecord(c->ev_d2h_done, c->d2h_s));
+    c->d2h_pending = true;
+    return GC_OK;
+}
+
+int claim_out(gc_ctx* c) {
+    if (c->d2h_pending) GC_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_d2h_done, 0));
     return GC_OK;
 }
 
@@ -177,6 +223,7 @@ int gc_destroy(gc_ctx* c) {
     if (!c) return GC_OK;
     cudaSetDevice(c->device);
     if (c->copy_s) cudaStreamSynchronize(c->copy_s);
+    if (c->d2h_s) cudaStreamSynchronize(c->d2h_s);
     cudaStreamSynchronize(c->stream);
     gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->stage_u, &c->stage_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
                         &c->dag_col, &c->dag_src, &c->dag_eid, &c->in_ptr, &c->in_pos, &c->in_src,
@@ -192,6 +239,9 @@ int gc_destroy(gc_ctx* c) {
         if (ev) cudaEventDestroy(ev);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->copy_s) cudaStreamDestroy(c->copy_s);
+    if (c->d2h_s) cudaStreamDestroy(c->d2h_s);
+    if (c->ev_out_ready) cudaEventDestroy(c->ev_out_ready);
+    if (c->ev_d2h_done) cudaEventDestroy(c->ev_d2h_done);
     if (c->ev_staged) cudaEventDestroy(c->ev_staged);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -358,6 +408,7 @@ int gc_edge_support(gc_ctx* c, uint32_t* support_out) {
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_edge_support before gc_build_csr");
     if (!support_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_edge_support: NULL output");
     cudaSetDevice(c->device);
+    GC_TRY(claim_out(c));   // a pending asynchronous read-back still reads out_tmp / out_tmp2
     GC_TRY(record(c, 4));
     GC_TRY(support_dag(c));
     GC_TRY(ensure(c, c->out_tmp, (size_t)c->m * sizeof(uint32_t)));
@@ -376,6 +427,7 @@ int gc_ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss before gc_build_csr");
     if (!alive_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_ktruss: NULL output");
     cudaSetDevice(c->device);
+    GC_TRY(claim_out(c));   // a pending asynchronous read-back still reads out_tmp / out_tmp2
     return ktruss(c, k, alive_out, m_alive);
 }
 
@@ -385,7 +437,30 @@ int gc_ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* supp
     if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss_analysis: k must be >= 2 (P:280)");
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss_analysis before gc_build_csr");
     cudaSetDevice(c->device);
+    GC_TRY(claim_out(c));   // a pending asynchronous read-back still reads out_tmp / out_tmp2
     return ktruss_analysis(c, k, triangles, support_out, alive_out, m_alive);
+}
+
+int gc_ktruss_analysis_async(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
+                             int64_t* m_alive) {
+    GC_TRY(check_ctx(c));
+    if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss_analysis_async: k must be >= 2 (P:280)");
+    if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss_analysis_async before gc_build_csr");
+    cudaSetDevice(c->device);
+    GC_TRY(claim_out(c));   // a pending asynchronous read-back still reads out_tmp / out_tmp2
+    c->async_out = true;
+    const int rc = ktruss_analysis(c, k, triangles, support_out, alive_out, m_alive);
+    c->async_out = false;
+    return rc;
+}
+
+int gc_wait(gc_ctx* c) {
+    GC_TRY(check_ctx(c));
+    cudaSetDevice(c->device);
+    if (c->d2h_s) GC_CUDA(c, cudaStreamSynchronize(c->d2h_s));
+    if (c->copy_s) GC_CUDA(c, cudaStreamSynchronize(c->copy_s));
+    c->d2h_pending = false;
+    return GC_OK;
 }
 
 int gc_truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
@@ -393,6 +468,7 @@ int gc_truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_truss_decomposition before gc_build_csr");
     if (!kmax || (!tau_out && c->m > 0)) return fail(c, GC_ERR_INVALID, "gc_truss_decomposition: NULL output");
     cudaSetDevice(c->device);
+    GC_TRY(claim_out(c));   // a pending asynchronous read-back still reads out_tmp / out_tmp2
     return truss_decomposition(c, tau_out, kmax);
 }
 

@@ -82,6 +82,10 @@ struct gc_ctx {
     int64_t stage_nnz = -1;          // >= 0: a staged list waits for the next gc_build_csr
     cudaStream_t copy_s = nullptr;   // library-owned copy stream of gc_stage_edges (lazy)
     cudaEvent_t ev_staged = nullptr;
+    cudaStream_t d2h_s = nullptr;    // library-owned read-back stream of gc_ktruss_analysis_async (lazy)
+    cudaEvent_t ev_out_ready = nullptr, ev_d2h_done = nullptr;
+    bool d2h_pending = false;        // out_tmp / out_tmp2 are being read back
+    bool async_out = false;          // the running call delivers per-edge outputs asynchronously
     int64_t nnz = 0;
 
     // graph sizes
@@ -157,6 +161,7 @@ struct gc_ctx {
     // pinned host scratch
     void* hpin = nullptr;
     size_t hpin_cap = 0;
+    void* hpin_dev = nullptr;        // hpin mapped into the device address space (read_small)
 
     // events
     cudaEvent_t ev[14] = {};   // 0-7 phases; 8-13 peel sub-phases (kernel / scan / compaction)
@@ -180,6 +185,14 @@ int sync(gc_ctx* c);
 // copy nbytes from device src to a caller pointer (host or device)
 int copy_out(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes);
 int copy_in(gc_ctx* c, void* dst_dev, const void* src, size_t nbytes);
+// per-edge output staged in out_tmp / out_tmp2 -> caller: on the context
+// stream, or on the read-back stream when c->async_out is set
+int copy_out_staged(gc_ctx* c, void* dst, const void* src_dev, size_t nbytes);
+// the context stream waits for a pending asynchronous read-back (before out_tmp / out_tmp2 are rewritten)
+int claim_out(gc_ctx* c);
+// a few bytes device -> the page-locked scratch c->hpin, ordered on the
+// context stream, without a copy engine
+int read_small(gc_ctx* c, void* host_dst, const void* src_dev, size_t nbytes);
 float elapsed(gc_ctx* c, int a, int b);
 int record(gc_ctx* c, int i);
 

@@ -675,7 +675,7 @@ int build_sym(gc_ctx* c) {
     if (n > 0)
         GC_LAUNCH(c, k_long_rows, grid_for(n), kThreads, 0, c->sym_ptr.as<int64_t>(), n, c->long_rows.as<int32_t>(),
                   cnt);
-    GC_CUDA(c, cudaMemcpyAsync(c->hpin, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, c->hpin, cnt, sizeof(int)));
     GC_TRY(sync(c));
     c->nlong = *static_cast<int*>(c->hpin);
     c->sym_ready = true;
@@ -783,7 +783,7 @@ static int peel_round_grouped(gc_ctx* c, const int32_t* front, int nf, const Pol
     Lt.nfront_dev = cnts + 1;
     GC_TRY(launch_peel(c, 148 * 8, Lt, pol, -1));
     int32_t* h = static_cast<int32_t*>(c->hpin);
-    GC_CUDA(c, cudaMemcpyAsync(h + 8, cnts, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h + 8, cnts, sizeof(int)));
     GC_TRY(sync(c));
     const int nh = h[8];
     if (nh == 0) return GC_OK;
@@ -848,9 +848,9 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
               len, thr, *round, c->front_a.as<int32_t>(), cnt,
               level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem, min_rest);
     GC_TRY(record(c, 11));
-    GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    GC_CUDA(c, cudaMemcpyAsync(h + 2, zrem, 8, cudaMemcpyDeviceToHost, c->stream));
-    GC_CUDA(c, cudaMemcpyAsync(h + 4, min_rest, 4, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, cnt, sizeof(int)));
+    GC_TRY(read_small(c, h + 2, zrem, 8));
+    GC_TRY(read_small(c, h + 4, min_rest, 4));
     GC_TRY(sync(c));
     c->stats.scan_ms += elapsed(c, 10, 11);
     {
@@ -889,8 +889,8 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             GC_TRY(record(c, 9));
             ++*round;
             cur = nxt;
-            GC_CUDA(c, cudaMemcpyAsync(h, counts[cur], sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-            GC_CUDA(c, cudaMemcpyAsync(h + 2, acc, 16, cudaMemcpyDeviceToHost, c->stream));
+            GC_TRY(read_small(c, h, counts[cur], sizeof(int)));
+            GC_TRY(read_small(c, h + 2, acc, 16));
             GC_TRY(sync(c));
             c->stats.peel_kernel_ms += elapsed(c, 8, 9);
             memcpy(done, h + 2, 16);
@@ -917,8 +917,8 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             cur = nxt;
         }
         GC_TRY(record(c, 9));
-        GC_CUDA(c, cudaMemcpyAsync(h, counts[cur], sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        GC_CUDA(c, cudaMemcpyAsync(h + 2, acc, 16, cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(read_small(c, h, counts[cur], sizeof(int)));
+        GC_TRY(read_small(c, h + 2, acc, 16));
         GC_TRY(sync(c));
         c->stats.peel_kernel_ms += elapsed(c, 8, 9);
         memcpy(done, h + 2, 16);
@@ -981,7 +981,7 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         if (nccl) GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
         GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
         GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, front, cnt);
-        GC_CUDA(c, cudaMemcpyAsync(h, cnt, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        GC_TRY(read_small(c, h, cnt, sizeof(int)));
         GC_TRY(sync(c));
         const int nf = h[0];
         if (nf == 0) break;
@@ -1054,13 +1054,12 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
         // collective on every rank whatever the output pointers (SPMD callers may differ in NULLs)
         if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(hits), 1));
         if (triangles)
-            GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 512, hits, 8, cudaMemcpyDeviceToHost,
-                                       c->stream));
+            GC_TRY(read_small(c, static_cast<char*>(c->hpin) + 512, hits, 8));
     }
     if (support_out && m > 0) {             // supports before the peel consumes them
         GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
         GC_TRY(scatter_canonical_u32(c, c->sup.as<uint32_t>(), c->out_tmp.as<uint32_t>()));
-        GC_TRY(copy_out(c, support_out, c->out_tmp.p, (size_t)m * 4));
+        GC_TRY(copy_out_staged(c, support_out, c->out_tmp.p, (size_t)m * 4));
     }
     GC_TRY(record(c, 2));
     int64_t removed = 0;
@@ -1083,9 +1082,8 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
                           (uint32_t)(k - 2), c->alive.as<uint8_t>(), kept);
                 GC_TRY(scatter_canonical_u8(c, c->alive.as<uint8_t>(), c->out_tmp2.as<uint8_t>()));
             }
-            if (alive_out) GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
-            GC_CUDA(c, cudaMemcpyAsync(static_cast<char*>(c->hpin) + 520, kept, 8, cudaMemcpyDeviceToHost,
-                                       c->stream));
+            if (alive_out) GC_TRY(copy_out_staged(c, alive_out, c->out_tmp2.p, (size_t)m));
+            GC_TRY(read_small(c, static_cast<char*>(c->hpin) + 520, kept, 8));
             GC_TRY(sync(c));
             removed = m - (int64_t)*reinterpret_cast<uint64_t*>(static_cast<char*>(c->hpin) + 520);
         }
@@ -1106,7 +1104,7 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
             } else {
                 GC_TRY(scatter_canonical_u8(c, c->alive.as<uint8_t>(), c->out_tmp2.as<uint8_t>()));
             }
-            GC_TRY(copy_out(c, alive_out, c->out_tmp2.p, (size_t)m));
+            GC_TRY(copy_out_staged(c, alive_out, c->out_tmp2.p, (size_t)m));
         }
     }
     GC_TRY(record(c, 1));

@@ -792,7 +792,7 @@ int prepare_tasks(gc_ctx* c) {
     tmp = c->cub_tmp.cap;
     GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cost, c->in_cost.as<int64_t>(), m + 1, c->stream));
     c->stats.lib_launches += 2;
-    GC_CUDA(c, cudaMemcpyAsync(h, c->in_cost.as<int64_t>() + m, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, c->in_cost.as<int64_t>() + m, 8));
     GC_TRY(sync(c));
     c->total_cost = h[0];
     if (c->total_cost == 0) {
@@ -816,7 +816,7 @@ int prepare_tasks(gc_ctx* c) {
     tmp = c->cub_tmp.cap;
     GC_CUDA(c, cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, iota, flags, sel, d_nsel, m, c->stream));
     c->stats.lib_launches += 2;
-    GC_CUDA(c, cudaMemcpyAsync(h, d_nsel, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, d_nsel, 8));
     GC_TRY(sync(c));
     const int64_t nt = h[0];
     unsigned long long* hist = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 160);
@@ -834,7 +834,7 @@ int prepare_tasks(gc_ctx* c) {
     GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
                                                c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
     c->stats.lib_launches += 3;
-    GC_CUDA(c, cudaMemcpyAsync(h, hist, 4 * 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, h, hist, 4 * 8));
     GC_TRY(sync(c));
     int64_t off = 0;
     for (int k = 0; k < 4; ++k) {
@@ -964,7 +964,7 @@ int triangle_count(gc_ctx* c, uint64_t* out) {
     GC_TRY(record(c, 7));
     if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(count), 1));
     GC_TRY(record(c, 3));
-    GC_CUDA(c, cudaMemcpyAsync(c->hpin, count, 8, cudaMemcpyDeviceToHost, c->stream));
+    GC_TRY(read_small(c, c->hpin, count, 8));
     GC_TRY(sync(c));
     *out = *static_cast<uint64_t*>(c->hpin);
     c->stats.tc_ms = elapsed(c, 2, 3);

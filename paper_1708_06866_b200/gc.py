@@ -47,7 +47,7 @@ GC_OPT_OVERLAP = 13
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "gc_create", "gc_destroy", "gc_last_error", "gc_nccl_unique_id", "gc_comm_init",
-    "gc_comm_init_loopback", "gc_load_edges", "gc_stage_edges", "gc_build_csr", "gc_num_vertices", "gc_num_edges",
+    "gc_comm_init_loopback", "gc_load_edges", "gc_stage_edges", "gc_build_csr", "gc_ktruss_analysis_async", "gc_wait", "gc_num_vertices", "gc_num_edges",
     "gc_get_edges", "gc_triangle_count", "gc_edge_support", "gc_ktruss", "gc_ktruss_analysis",
     "gc_truss_decomposition", "gc_list_triangles",
     "gc_set_option", "gc_get_stats", "gc_reset_stats", "gc_partition_bounds",
@@ -107,6 +107,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "gc_ktruss": ([_vp, _i32, _vp, ctypes.POINTER(_i64)], ctypes.c_int),
         "gc_ktruss_analysis": ([_vp, _i32, ctypes.POINTER(ctypes.c_uint64), _vp, _vp, ctypes.POINTER(_i64)],
                                ctypes.c_int),
+        "gc_ktruss_analysis_async": ([_vp, _i32, ctypes.POINTER(ctypes.c_uint64), _vp, _vp, ctypes.POINTER(_i64)],
+                                     ctypes.c_int),
+        "gc_wait": ([_vp], ctypes.c_int),
         "gc_truss_decomposition": ([_vp, _vp, ctypes.POINTER(_i32)], ctypes.c_int),
         "gc_list_triangles": ([_vp, _vp, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
         "gc_set_option": ([_vp, ctypes.c_int, _i64], ctypes.c_int),
@@ -174,6 +177,7 @@ class Context:
             raise GcError(rc, self._L.gc_last_error(None).decode())
         self._h = h
         self._staged = None
+        self._pending_out = None
         self.device = device
         self._keep = []
 
@@ -282,6 +286,22 @@ class Context:
         self._check(self._L.gc_ktruss_analysis(self._h, int(k), ctypes.byref(t), _vp(_ptr(support_out)),
                                                _vp(_ptr(mask_out)), ctypes.byref(ma)))
         return int(t.value), support_out, mask_out, int(ma.value)
+
+    def ktruss_analysis_async(self, k: int, support_out, mask_out):
+        """gc_ktruss_analysis_async: as ktruss_analysis into caller buffers
+        (page-locked host or device) whose contents are valid only after
+        wait().  Returns (triangles, m_alive) at once."""
+        t = ctypes.c_uint64()
+        ma = _i64()
+        self._check(self._L.gc_ktruss_analysis_async(self._h, int(k), ctypes.byref(t), _vp(_ptr(support_out)),
+                                                     _vp(_ptr(mask_out)), ctypes.byref(ma)))
+        self._pending_out = (support_out, mask_out)
+        return int(t.value), int(ma.value)
+
+    def wait(self):
+        """gc_wait: every asynchronous copy of this context is done."""
+        self._check(self._L.gc_wait(self._h))
+        self._pending_out = None
 
     def truss_decomposition(self, out=None):
         if out is None:

@@ -670,6 +670,40 @@ def test_staged_edges(gcmod):
         assert c.num_edges() == 0 and c.triangle_count() == 0
 
 
+def test_async_outputs(gcmod):
+    """gc_ktruss_analysis_async: scalars at return, per-edge outputs after
+    gc_wait; pipelined with gc_stage_edges; a following synchronous call
+    waits for the pending read-back before reusing its staging buffers."""
+    import torch
+    ga = gen.rmat(12, 16, seed=51)
+    gb = gen.rmat(11, 8, seed=52)
+    oa, ob = oracle.OracleGraph(*ga), oracle.OracleGraph(*gb)
+    with gcmod.Context(0) as c:
+        c.load_edges(*ga)
+        c.build_csr()
+        m = c.num_edges()
+        hs = torch.empty(m, dtype=torch.int32).pin_memory()
+        hm = torch.empty(m, dtype=torch.uint8).pin_memory()
+        T, ma = c.ktruss_analysis_async(4, hs, hm)
+        want, _ = oa.ktruss(4)
+        assert T == oa.triangle_count() and ma == int(want.sum())
+        c.stage_edges(*gb)                          # next graph's copy while the read-back runs
+        sup_sync = c.edge_support()                 # waits for the pending read-back first
+        c.wait()
+        assert np.array_equal(hs.numpy().view(np.uint32), oa.support()) and np.array_equal(hm.numpy(), want)
+        assert np.array_equal(sup_sync, oa.support())
+        c.build_csr()
+        mb = c.num_edges()
+        ds = torch.empty(mb, dtype=torch.int32, device="cuda")
+        dm = torch.empty(mb, dtype=torch.uint8, device="cuda")
+        T, ma = c.ktruss_analysis_async(3, ds, dm)  # device outputs
+        c.wait()
+        want, _ = ob.ktruss(3)
+        assert T == ob.triangle_count() and ma == int(want.sum())
+        assert np.array_equal(ds.cpu().numpy().view(np.uint32), ob.support())
+        assert np.array_equal(dm.cpu().numpy(), want)
+
+
 def test_device_pointers_and_determinism(ctx):
     import torch
     u, v = gen.rmat(12, 16, seed=21)
