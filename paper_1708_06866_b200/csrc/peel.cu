@@ -314,27 +314,68 @@ constexpr int kSerialRow = 8;
 #define GC_PEEL_GMAX 8   // frontier edges per warp at most (8: K13 kernel 226 -> 78 ms, C4 +0.7 %)
 #endif
 
+
+// Branch-free lower bounds of two targets in one sorted range, in lockstep:
+// the halving sequence does not depend on the targets, so the two searches'
+// loads are independent and in flight together (the peel's searches are
+// latency-bound: C4 / C5 decomposition kernels -15 % / -12 %; a generic
+// N-target version with register arrays needed more registers and was slower
+// at 2, 3 and 4 targets).  r = smallest i in [lo, hi) with a[i] >= x, hi if none.
+__device__ __forceinline__ void lower_bound_x2(const int32_t* __restrict__ a, int64_t lo, int64_t hi, int32_t x0,
+                                               int32_t x1, int64_t& r0, int64_t& r1) {
+    int64_t n = hi - lo;
+    if (n <= 0) {
+        r0 = r1 = lo;
+        return;
+    }
+    int64_t p0 = lo, p1 = lo;
+    while (n > 1) {
+        const int64_t half = n >> 1;
+        const int32_t v0 = __ldg(a + p0 + half), v1 = __ldg(a + p1 + half);
+        p0 = v0 < x0 ? p0 + half : p0;
+        p1 = v1 < x1 ? p1 + half : p1;
+        n -= half;
+    }
+    r0 = p0 + (__ldg(a + p0) < x0);
+    r1 = p1 + (__ldg(a + p1) < x1);
+}
+
 template <class Pol>
 __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol, int e, uint32_t live, int64_t a0,
                                               int64_t a1, int64_t b0, int64_t b1, int lane) {
     uint32_t found = 0;
-    for (int64_t base = a0; base < a1 && found < live; base += 32) {
-        const int64_t i = base + lane;
-        bool tri = false;
-        int f = -1, g = -1;
-        if (i < a1) {
-            f = __ldg(A.sym_eid + i);
-            if (f != e && A.alive[f]) {
-                const int32_t w = __ldg(A.sym_col + i);
-                const int64_t j = lower_bound_i32(A.sym_col, b0, b1, w);
-                if (j < b1 && __ldg(A.sym_col + j) == w) {
-                    g = __ldg(A.sym_eid + j);
-                    tri = A.alive[g] != 0;
-                }
+    // two 32-entry chunks of the shorter row per step, their searches interleaved
+    for (int64_t base = a0; base < a1 && found < live; base += 64) {
+        const int64_t i0 = base + lane, i1 = base + 32 + lane;
+        int f0 = -1, f1 = -1;
+        int32_t w0 = INT32_MAX, w1 = INT32_MAX;
+        if (i0 < a1) {
+            f0 = __ldg(A.sym_eid + i0);
+            w0 = __ldg(A.sym_col + i0);
+        }
+        if (i1 < a1) {
+            f1 = __ldg(A.sym_eid + i1);
+            w1 = __ldg(A.sym_col + i1);
+        }
+        const bool want0 = i0 < a1 && f0 != e && A.alive[f0];
+        const bool want1 = i1 < a1 && f1 != e && A.alive[f1];
+        bool tri0 = false, tri1 = false;
+        int g0 = -1, g1 = -1;
+        if (want0 || want1) {
+            int64_t j0, j1;
+            lower_bound_x2(A.sym_col, b0, b1, w0, w1, j0, j1);
+            if (want0 && j0 < b1 && __ldg(A.sym_col + j0) == w0) {
+                g0 = __ldg(A.sym_eid + j0);
+                tri0 = A.alive[g0] != 0;
+            }
+            if (want1 && j1 < b1 && __ldg(A.sym_col + j1) == w1) {
+                g1 = __ldg(A.sym_eid + j1);
+                tri1 = A.alive[g1] != 0;
             }
         }
-        found += __popc(__ballot_sync(0xffffffffu, tri));
-        if (tri) destroy(pol, e, f, g);
+        found += __popc(__ballot_sync(0xffffffffu, tri0)) + __popc(__ballot_sync(0xffffffffu, tri1));
+        if (tri0) destroy(pol, e, f0, g0);
+        if (tri1) destroy(pol, e, f1, g1);
     }
 }
 
@@ -371,7 +412,7 @@ __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
         const int64_t chunks = (a1 - a0 + 31) / 32;
         const int64_t c0 = chunks * slice / wpe, c1 = chunks * (slice + 1) / wpe;
         if (c1 > c0)
-            peel_one_warp(A, pol, e, 0xFFFFFFFFu, a0 + 32 * c0, min(a1, a0 + 32 * c1), b0, b1, lane);
+            peel_one_warp<Pol>(A, pol, e, 0xFFFFFFFFu, a0 + 32 * c0, min(a1, a0 + 32 * c1), b0, b1, lane);
         return;
     }
     const int G = (int)max((int64_t)1, min((int64_t)GC_PEEL_GMAX, nfront / warps));     // edges per warp
@@ -414,7 +455,7 @@ __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
         while (coop) {                                  // the whole warp, one edge at a time
             const int src = __ffs(coop) - 1;
             coop &= coop - 1;
-            peel_one_warp(A, pol, __shfl_sync(0xffffffffu, e, src), __shfl_sync(0xffffffffu, live, src),
+            peel_one_warp<Pol>(A, pol, __shfl_sync(0xffffffffu, e, src), __shfl_sync(0xffffffffu, live, src),
                           __shfl_sync(0xffffffffu, a0, src), __shfl_sync(0xffffffffu, a1, src),
                           __shfl_sync(0xffffffffu, b0, src), __shfl_sync(0xffffffffu, b1, src), lane);
         }
