@@ -549,9 +549,8 @@ struct SmemBitmap {
     __device__ __forceinline__ void credit(int hd, uint32_t*) const {
         if (!SUP) return;
         const uint32_t x = (uint32_t)hd;
-        const uint32_t word = bits[x >> 5];
-        const uint32_t lo = (x & 32) ? bits[(x >> 5) - 1] : 0u;   // lower word of the chunk
-        const int j = (int)pre[x >> 6] + __popc(lo) + __popc(word & ((1u << (x & 31)) - 1u));
+        const uint64_t chunk = reinterpret_cast<const uint64_t*>(bits)[x >> 6];   // one 64-bit LDS
+        const int j = (int)pre[x >> 6] + __popcll(chunk & ((1ull << (x & 63)) - 1ull));
         atomicAdd(cnt + j, 1u);
     }
 };

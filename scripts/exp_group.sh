@@ -1,2 +1,5 @@
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu 2>&1 | tail -1
-for cfg in C4 C5; do timeout 300 python scripts/run_decomp.py --config $cfg --ks 4,5,6 2>&1 | grep -E "decomposition|ktruss" | cut -c1-150; done
+for lib in build_var/prev2/libgc.so paper_1708_06866_b200/libgc.so build_var/prev2/libgc.so paper_1708_06866_b200/libgc.so; do
+echo $lib
+GC_LIB_PATH=$lib python scripts/run_tc.py --config C4 --reps 3 --what tc,support | tail -1 | cut -c1-130
+done
+python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "c3 or c4 or forced or heavy or golden or fuzz" 2>&1 | tail -1
