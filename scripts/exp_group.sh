@@ -1,5 +1,3 @@
-for lib in build_var/prev2/libgc.so paper_1708_06866_b200/libgc.so build_var/prev2/libgc.so paper_1708_06866_b200/libgc.so; do
-echo $lib
-GC_LIB_PATH=$lib python scripts/run_tc.py --config C4 --reps 3 --what tc,support | tail -1 | cut -c1-130
+for o in "2=32768" "2=65536" "2=131072" "2=16384" "5=32" "5=64" "5=96"; do
+echo $o; python scripts/run_tc.py --config C4 --reps 3 --what tc,support --opt $o | tail -1 | cut -c1-130
 done
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "c3 or c4 or forced or heavy or golden or fuzz" 2>&1 | tail -1
