@@ -240,7 +240,8 @@ typedef enum gc_option {
                                  side stream that overlaps the block-task kernels and is
                                  joined before the call returns (default); 0: one stream */
     GC_OPT_GROUP_PEEL = 12,   /* peeler: rounds with at least this many frontier edges
-                                 (default 2^20; 0: never) -- a dense core collapsing -- group
+                                 (default 0: never; 2^20 was the earlier default, slower since
+                                 the per-edge search keeps two searches in flight) group
                                  their heavy edges by the endpoint with the longer live row,
                                  whose row is staged once per group as a shared-memory bitmap */
     GC_OPT_GROUP_HEAVY = 14,  /* ... heavy = shorter live row at least this long (default

@@ -142,7 +142,7 @@ struct gc_ctx {
     gcx::Buf batch_slot;   // int64 per-block next-batch slots of the block-class kernels
     gcx::Buf grp_keys, grp_vals, grp_starts, grp_flags, grp_light;   // grouped dense-core rounds
     int64_t peel_big = getenv("GC_PEEL_BIG") ? atoll(getenv("GC_PEEL_BIG")) : (1 << 20);   // frontier size from which k_peel runs its 48-register build
-    int group_peel = 1 << 20;   // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
+    int group_peel = 0;         // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
     int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped
     gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)
     int64_t alist_n = -1;       // -1: no list (scan every edge)
