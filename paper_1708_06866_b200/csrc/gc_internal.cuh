@@ -141,7 +141,9 @@ struct gc_ctx {
     int nlong = 0;
     gcx::Buf batch_slot;   // int64 per-block next-batch slots of the block-class kernels
     gcx::Buf grp_keys, grp_vals, grp_starts, grp_flags, grp_light;   // grouped dense-core rounds
-    int64_t peel_big = getenv("GC_PEEL_BIG") ? atoll(getenv("GC_PEEL_BIG")) : (1 << 20);   // frontier size from which k_peel runs its 48-register build
+    // frontier size from which k_peel runs its 64-register build (diagnostics; default never: with two
+    // searches in flight per lane the full-occupancy 32-register build wins at every frontier size)
+    int64_t peel_big = getenv("GC_PEEL_BIG") ? atoll(getenv("GC_PEEL_BIG")) : INT64_MAX;
     int group_peel = 0;         // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
     int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped
     gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)

@@ -379,11 +379,12 @@ __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol,
     }
 }
 
-// MINB: two builds of the kernel.  MINB = 1 (48 registers) for big frontiers,
-// whose grouped lanes need the registers; MINB = 8 (32 registers, the SM's
-// 64 warps) for the small rounds that dominate a decomposition, where the
-// searches are latency-bound (C4 / C5 decomposition kernels -29 % / -25 %,
-// but a 20 M-edge first round of ktruss(5) 2.6x slower).
+// MINB: the register budget.  MINB = 8 (32 registers, the SM's 64 warps) is
+// the build that runs: the searches are latency-bound, and with two of them
+// in flight per lane it wins at every frontier size (C4 / C5 decomposition
+// kernels 1.50 -> 1.40 s / 19.4 -> 17.4 s, C4 ktruss(6) peel 119 -> 99 ms
+// against MINB = 1 for frontiers of 2^20 edges and more).  MINB = 1 stays
+// reachable through GC_PEEL_BIG for A/B runs.
 template <class Pol, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
     const int lane = threadIdx.x & 31;

@@ -1,2 +1,2 @@
 python -m pytest tests/test_parity_gpu.py -q -x -m gpu 2>&1 | tail -1
-python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_tmp.log 2>&1; echo rc=$?
+for cfg in C3 C4 C5 K13; do timeout 300 python scripts/run_decomp.py --config $cfg --ks 4,5,6 2>&1 | grep -E "decomposition|ktruss" | cut -c1-150; done

@@ -534,6 +534,28 @@ def test_grouped_dense_core_rounds(gcmod, heavy):
                 assert np.array_equal(tau, want_tau) and kmax == want_kmax
 
 
+def test_peel_register_builds(gcmod, monkeypatch):
+    """Both register budgets of the peel kernel (GC_PEEL_BIG=1: the 64-register
+    build for every round; default: the 32-register build) give the oracle's
+    k-trusses and decomposition on C1 and an R-MAT s12."""
+    for env in ("1", None):
+        if env:
+            monkeypatch.setenv("GC_PEEL_BIG", env)
+        else:
+            monkeypatch.delenv("GC_PEEL_BIG", raising=False)
+        for u, v in [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=61)]:
+            g = oracle.OracleGraph(u, v)
+            with gcmod.Context(0) as c:
+                c.load_edges(u, v)
+                c.build_csr()
+                for k in (4, 6):
+                    want, _ = g.ktruss(k)
+                    assert np.array_equal(c.ktruss(k)[0], want), (env, k)
+                tau, kmax = c.truss_decomposition()
+                want_tau, want_kmax = g.truss_decomposition()
+                assert np.array_equal(tau, want_tau) and kmax == want_kmax, env
+
+
 @pytest.mark.parametrize("parts", [1, 2, 5])
 def test_partitioned_peeler_c1_and_fixtures(gcmod, parts):
     """The multi-GPU peeler (removed-edge bitmap per round, owner-only
