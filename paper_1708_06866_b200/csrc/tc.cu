@@ -175,7 +175,7 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
         uint8_t f = 0;
         if (ch > 0) {
             if (i == in_ptr[v]) f = 1;
-            else if (floor_div(pref[i], ch) != floor_div(pref[i - 1], ch)) f = 1;
+            else if (floor_div(pref[i], ch) * ch > pref[i - 1]) f = 1;   // a multiple of ch in (pref[i-1], pref[i]]
             else if (parts > 1 && (pref[i] * parts) / total != (pref[i - 1] * parts) / total) f = 1;
         }
         flag[i] = f;
