@@ -19,6 +19,9 @@
 
 #include <algorithm>
 
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
 #include "gc_internal.cuh"
 
 #ifndef GC_SPLIT_SORT1
@@ -71,11 +74,14 @@ __global__ void k_pack_split(const int32_t* __restrict__ u, const int32_t* __res
     }
 }
 
-__global__ void k_join_keys(const uint32_t* __restrict__ lo, const uint32_t* __restrict__ hi, int64_t nnz, int b,
-                            uint64_t* __restrict__ keys) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
-        keys[i] = ((uint64_t)lo[i] << b) | hi[i];
-}
+// (lo, hi) halves of the sorted pairs -> the canonical 64-bit key, on the fly
+struct JoinKey {
+    const uint32_t* lo;
+    const uint32_t* hi;
+    int b;
+    __host__ __device__ uint64_t operator()(int64_t i) const { return ((uint64_t)lo[i] << b) | hi[i]; }
+};
+
 
 __global__ void k_degrees(const uint64_t* __restrict__ canon, int64_t m, int b, int32_t* __restrict__ deg,
                           int32_t* __restrict__ first, int32_t* __restrict__ last) {
@@ -326,6 +332,7 @@ int build_csr(gc_ctx* c) {
         GC_TRY(ensure(c, c->keys_a, (size_t)nnz * 8));
         GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
         const uint64_t sent = (2 * b >= 64) ? ~0ULL : ((1ULL << (2 * b)) - 1);
+        bool joined_done = false;
         if (GC_SPLIT_SORT1 && b <= 31) {
             // (lo, hi) order by two stable 32-bit pair sorts, hi then lo: the same
             // bytes per pass as one 64-bit key sort, with 32-bit digits passes
@@ -342,8 +349,20 @@ int build_csr(gc_ctx* c) {
             GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hi_a, hi_b, lo_a, lo_b, nnz, 0, b, c->stream));
             GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, lo_b, lo_a, hi_b, hi_a, nnz, 0, b, c->stream));
             c->stats.lib_launches += 2 * (2 + (b + 7) / 8);
-            // joined 64-bit keys into keys_b (lo_b/hi_b are consumed)
-            GC_LAUNCH(c, k_join_keys, grid_for(nnz), kThreads, 0, lo_a, hi_a, nnz, b, c->keys_b.as<uint64_t>());
+            // the unique pass reads the two halves joined on the fly (no 64-bit key array)
+            GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
+            int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
+            auto joined = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                          JoinKey{lo_a, hi_a, b});
+            size_t tmp2 = 0;
+            GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp2, joined, c->canon.as<uint64_t>(), d_nsel, nnz,
+                                                 c->stream));
+            GC_TRY(ensure(c, c->cub_tmp, tmp2));
+            tmp2 = c->cub_tmp.cap;
+            GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp2, joined, c->canon.as<uint64_t>(), d_nsel, nnz,
+                                                 c->stream));
+            c->stats.lib_launches += 2;
+            joined_done = true;
         } else {
             GC_LAUNCH(c, k_pack, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz, b,
                       sent, c->keys_a.as<uint64_t>());
@@ -351,14 +370,16 @@ int build_csr(gc_ctx* c) {
         }
         GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
         int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
-        size_t tmp = 0;
-        GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(), d_nsel,
-                                             nnz, c->stream));
-        GC_TRY(ensure(c, c->cub_tmp, tmp));
-        tmp = c->cub_tmp.cap;
-        GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
-                                             d_nsel, nnz, c->stream));
-        c->stats.lib_launches += 2;
+        if (!joined_done) {
+            size_t tmp = 0;
+            GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
+                                                 d_nsel, nnz, c->stream));
+            GC_TRY(ensure(c, c->cub_tmp, tmp));
+            tmp = c->cub_tmp.cap;
+            GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp, c->keys_b.as<uint64_t>(),
+                                                 c->canon.as<uint64_t>(), d_nsel, nnz, c->stream));
+            c->stats.lib_launches += 2;
+        }
         GC_TRY(read_small(c, h, d_nsel, 8));
         GC_TRY(sync(c));
         int64_t nsel = h[0];
