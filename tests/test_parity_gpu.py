@@ -756,3 +756,16 @@ def test_errors(ctx, gcmod):
         with pytest.raises(gcmod.GcError) as e:
             c2.triangle_count()
         assert e.value.code == gcmod.GC_ERR_STATE
+        c2.wait()                                            # nothing pending: a no-op
+        with pytest.raises(gcmod.GcError) as e:              # NULL source with nnz > 0
+            c2._check(c2._L.gc_stage_edges(c2._h, None, None, 5))
+        assert e.value.code == gcmod.GC_ERR_INVALID
+        with pytest.raises(gcmod.GcError) as e:              # staged, not built yet
+            c2.stage_edges(np.array([0, 1], np.int32), np.array([1, 2], np.int32))
+            c2.num_edges()
+        assert e.value.code == gcmod.GC_ERR_STATE
+        c2.build_csr()
+        assert c2.num_edges() == 2
+        with pytest.raises(gcmod.GcError) as e:
+            c2.ktruss_analysis_async(1, np.empty(2, np.uint32), np.empty(2, np.uint8))
+        assert e.value.code == gcmod.GC_ERR_INVALID
