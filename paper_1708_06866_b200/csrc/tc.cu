@@ -73,12 +73,16 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #define GC_SUP_MINB 4                       // ... and resident blocks per SM (register budget)
 #endif
 #ifndef GC_HUGE_WARPS_TC
-#define GC_HUGE_WARPS_TC 16                 // huge-head kernels (class 3): warps per block sharing the
+#define GC_HUGE_WARPS_TC 20                 // huge-head kernels (class 3): warps per block sharing the
 #endif                                      // table (1-3 resident blocks per SM: more warps hide latency)
 #ifndef GC_HUGE_WARPS_SUP
 #define GC_HUGE_WARPS_SUP 32
 #endif
 #define GC_HUGE_WARPS(S) ((S) ? GC_HUGE_WARPS_SUP : GC_HUGE_WARPS_TC)
+#ifndef GC_HUGE_MINB_TC
+#define GC_HUGE_MINB_TC 3                   // huge-head count kernel: resident blocks per SM to budget for (3 x 20 warps at
+                                            // 32 registers: C5 TC 520 -> 481 ms against 2 x 16 at 61)
+#endif
 #ifndef GC_TC_WARPS
 #define GC_TC_WARPS 12                      // heavy-head count kernel: warps per block (5 x 12 = 60 warps
                                             // at 32 registers: C4 51.0 -> 49.2 ms, C5 545 -> 523 ms)
@@ -594,7 +598,7 @@ struct GlobalProbe {
 
 template <bool SUP, bool HUGE>
 __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS),
-                                  HUGE ? 1 : (SUP ? GC_SUP_MINB : GC_TC_MINB))
+                                  HUGE ? (SUP ? 1 : GC_HUGE_MINB_TC) : (SUP ? GC_SUP_MINB : GC_TC_MINB))
     k_tc_block(KArgs a) {
     constexpr int BW = HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS;   // warps per block (= blockDim.x / 32)
     uint32_t* const smem = g_dsmem;
