@@ -1,5 +1,4 @@
-for lib in paper_1708_06866_b200/libgc.so build_var/h20m3/libgc.so; do
+for lib in paper_1708_06866_b200/libgc.so build_var/v4/libgc.so build_var/v4w12/libgc.so; do
 echo $lib
-GC_LIB_PATH=$lib python scripts/run_tc.py --config C5 --reps 2 --what tc | tail -1 | cut -c1-100
+GC_LIB_PATH=$lib python scripts/run_tc.py --config C4 --reps 3 --what tc,support | tail -1 | cut -c1-130
 done
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "huge or c5 or forced or large" 2>&1 | tail -1
