@@ -1,3 +1,1 @@
-python scripts/run_tc.py --config C4 --reps 3 --what tc,support | tail -1 | cut -c1-130
-python scripts/run_tc.py --config C5 --reps 2 --what tc,support | tail -1 | cut -c1-130
-python -m pytest tests/test_parity_gpu.py -q -x -m gpu 2>&1 | tail -1
+for o in "13=1" "13=0" "13=1" "13=0"; do echo $o; python scripts/run_tc.py --config C4 --reps 3 --what tc,support --opt $o | tail -1 | cut -c1-120; done
