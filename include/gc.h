@@ -234,8 +234,9 @@ typedef enum gc_option {
                                  16384-slot shared hash at load 1/2) search N+(v) in
                                  global memory instead (0..8192; testing) */
     GC_OPT_COMPACT = 10,      /* peeler: drop dead entries from the adjacency rows each
-                                 time the live edge count falls to 1/value of the last
-                                 compaction (default 2; 0 or 1: never; testing) */
+                                 time the live edge count falls to (value-1)/value of the
+                                 last compaction during gc_truss_decomposition (default 5,
+                                 i.e. 4/5; a single k-truss uses min(value, 2)); 0 or 1: never */
     GC_OPT_OVERLAP = 13,      /* 1: the warp-task intersection kernels run on a library
                                  side stream that overlaps the block-task kernels and is
                                  joined before the call returns (default); 0: one stream */

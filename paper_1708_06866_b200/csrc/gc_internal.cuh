@@ -151,7 +151,8 @@ struct gc_ctx {
     int64_t m_alive_h = 0;      // live edges (host mirror)
     int64_t compact_at = 0;     // live edges at the last compaction
     int trace = getenv("GC_PEEL_TRACE") ? atoi(getenv("GC_PEEL_TRACE")) : 0;   // diagnostics: 1 a line per batch, 2 per round
-    int compact_div = 2;        // compact when live edges fall to 1/compact_div (GC_OPT_COMPACT; <= 1 never)
+    int compact_div = 5;        // compact when live edges fall to (v-1)/v, v = compact_div (GC_OPT_COMPACT; <= 1 never)
+    bool decomp_running = false;   // a truss decomposition is peeling (compact_div applies; else at most 2)
     gcx::Buf alive;     // uint8[m] edge state: 0 removed, 1 alive, 2 / 3 in the frontier (peel.cu st_front)
     gcx::Buf front_a, front_b;  // int32[m] frontier lists
     gcx::Buf tau;       // int32[m]

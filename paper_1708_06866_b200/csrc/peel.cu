@@ -741,10 +741,15 @@ static int sym_refill(gc_ctx* c) {
 }
 
 // Drop dead entries from the rows once the live edge count has fallen to
-// 1/compact_div of what it was at the last compaction (or the start).
+// (compact_div - 1) / compact_div of what it was at the last compaction (or the start): the
+// searches re-read row sectors from DRAM, so denser rows pay (C4 / C5 decomposition kernel +
+// scan + compaction 1.55 / 19.0 s at 1/2, 1.44 / 18.1 s at 4/5).
 static int maybe_compact(gc_ctx* c) {
     if (!c->rows_live) return GC_OK;
-    if (c->compact_div <= 1 || c->m_alive_h <= 0 || c->m_alive_h * c->compact_div > c->compact_at) return GC_OK;
+    // compact once the live edges fall to (v - 1) / v of the last compaction, v = compact_div
+    // in a decomposition (many levels follow to repay it); a single k-truss keeps v <= 2
+    const int64_t v = c->decomp_running ? c->compact_div : std::min(c->compact_div, 2);
+    if (v <= 1 || c->m_alive_h <= 0 || c->m_alive_h * v > c->compact_at * (v - 1)) return GC_OK;
     const int64_t n = c->n, m = c->m;
     GC_TRY(record(c, 12));
     GC_LAUNCH(c, k_row_compact_warp, grid_for(n * 32), kThreads, 0, c->sym_ptr.as<int64_t>(),
@@ -1165,6 +1170,11 @@ int ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
 
 int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
     const int64_t m = c->m;
+    struct DecompFlag {
+        gc_ctx* c;
+        ~DecompFlag() { c->decomp_running = false; }
+    } flag{c};
+    c->decomp_running = true;
     GC_TRY(record(c, 0));
     GC_TRY(support_dag(c));
     GC_TRY(record(c, 2));

@@ -1,1 +1,2 @@
-for o in "13=1" "13=0" "13=1" "13=0"; do echo $o; python scripts/run_tc.py --config C4 --reps 3 --what tc,support --opt $o | tail -1 | cut -c1-120; done
+python -m pytest tests/test_parity_gpu.py -q -x -m gpu -k "c1 or c3 or compaction or fuzz or golden or register or partition or grouped" 2>&1 | tail -1
+for cfg in C4 C5; do timeout 300 python scripts/run_decomp.py --config $cfg --ks 4,5,6 2>&1 | grep -E "decomposition|ktruss" | cut -c1-170; done
