@@ -49,7 +49,7 @@ def _lib():
                                              i32p, i32p, i32p, ctypes.c_int]
         L.or_truss_decomposition.restype = ctypes.c_int64
         L.or_truss_sequential.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p,
-                                          i32p, u32p, i32p, i32p]
+                                          i32p, u32p, i32p, i32p, ctypes.c_int]
         L.or_truss_sequential.restype = ctypes.c_int64
         _LIB = L
     return _LIB
@@ -131,13 +131,20 @@ class OracleGraph:
         return tau[: self.m].copy(), int(kmax.value)
 
     # O-7
-    def truss_sequential(self, support: np.ndarray | None = None):
+    def truss_sequential(self, support: np.ndarray | None = None, consume: bool = False):
+        """O-7.  consume=True lets the peel use this graph's adjacency rows as
+        its live-row storage (no copy; the graph is unusable afterwards)."""
         if support is None:
             support = self.support()
         support = np.ascontiguousarray(support, dtype=np.uint32)
         tau = np.zeros(max(self.m, 1), dtype=np.int32)
         kmax = ctypes.c_int32(0)
-        _lib().or_truss_sequential(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p),
-                                   _p(self.ptr, i64p), _p(self.col, i32p), _p(self.eid, i32p),
-                                   _p(support, u32p), _p(tau, i32p), ctypes.byref(kmax))
+        r = _lib().or_truss_sequential(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p),
+                                       _p(self.ptr, i64p), _p(self.col, i32p), _p(self.eid, i32p),
+                                       _p(support, u32p), _p(tau, i32p), ctypes.byref(kmax),
+                                       1 if consume else 0)
+        if r < 0:
+            raise MemoryError("or_truss_sequential: out of memory (or m > 2^31-1)")
+        if consume:
+            self.col = self.eid = None
         return tau[: self.m].copy(), int(kmax.value)

@@ -151,6 +151,15 @@ static int64_t lower_bound32(const int32_t* a, int64_t lo, int64_t hi, int32_t x
     return lo;
 }
 
+/* First index in [lo, hi) with a[index] >= x, by exponential then binary
+ * search from lo (galloping: log of the distance moved). */
+static int64_t gallop32(const int32_t* a, int64_t lo, int64_t hi, int32_t x) {
+    int64_t prev = lo, step = 1;
+    while (lo < hi && a[lo] < x) { prev = lo + 1; lo += step; step <<= 1; }
+    if (lo > hi) lo = hi;
+    return lower_bound32(a, prev, lo, x);
+}
+
 static int64_t intersect_count(const int32_t* A, int64_t na, const int32_t* B, int64_t nb) {
     if (na == 0 || nb == 0) return 0;
     if (na > nb) { const int32_t* t = A; A = B; B = t; int64_t tn = na; na = nb; nb = tn; }
@@ -325,76 +334,150 @@ int64_t or_truss_decomposition(int64_t n, int64_t m, const int32_t* cu, const in
 }
 
 /* ------------------------------------------------------------------ O-7 --
- * Tier-2 decomposition: remove one edge at a time, always one of minimum
- * current support (bin-sort buckets as in Batagelj-Zaversnik k-core).  When
- * e = (a,b) is removed with current support s, tau(e) = s + 2; every live
- * triangle (e, f, g) loses e, so f and g each lose one unit of support,
- * unless already at e's level (they will be removed at the same level).
- * Sequential removal destroys each triangle exactly once.  Equal to O-6 by
- * uniqueness of the maximal k-truss.  sup_init: O-3 supports (m). */
+ * Tier-2 decomposition: remove one edge at a time, always
+ * one of minimum current support (bin-sort buckets as in Batagelj-Zaversnik
+ * k-core).  When e = (a,b) is removed with current support s, tau(e) = s + 2;
+ * every live triangle (e, f, g) loses e, so f and g each lose one unit of
+ * support, unless already at e's level (they will be removed at the same
+ * level).  Sequential removal destroys each triangle exactly once.  Equal to
+ * O-6 by uniqueness of the maximal k-truss (readings A2/A8).
+ *
+ * The live triangles through e are N_live(a) ∩ N_live(b), a plain sorted-list
+ * intersection: two-pointer merge, or a galloping search of the shorter row
+ * in the longer one when that is at least 32x longer (same set, fewer steps;
+ * the same rule as O-3).  Storage details that change neither the removal order
+ * nor the arithmetic: rows keep their live entries at the front (a row
+ * holding more than twice its live count + 16 drops its dead entries in
+ * place, keeping the order); an edge's support and bucket slot sit side by
+ * side (slot -1 = removed); the common neighbours of e are listed first and
+ * then applied in the same order (e's removal changes no other edge's state,
+ * so listing first is the same as applying while merging).
+ *
+ * sup_init: O-3 supports (m).  consume != 0: col/eid are used as the row
+ * storage and left scrambled (saves 8 B per stored entry at C4/C5); else they
+ * are copied.  Returns m, or -1 on OOM / m > INT32_MAX. */
+#ifndef O7_GALLOP
+#define O7_GALLOP 32
+#endif
+typedef struct { uint32_t s; int32_t pos; } o7_edge;
+
 int64_t or_truss_sequential(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
-                            const int64_t* ptr, const int32_t* col, const int32_t* eid,
-                            const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out) {
-    (void)n;
+                            const int64_t* ptr, int32_t* col_in, int32_t* eid_in,
+                            const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out, int consume) {
     if (m == 0) { *kmax_out = 0; return 0; }
-    uint32_t* S = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m);
-    uint32_t smax = 0;
-    for (int64_t e = 0; e < m; ++e) { S[e] = sup_init[e]; if (S[e] > smax) smax = S[e]; }
-    int64_t* bin = (int64_t*)calloc((size_t)smax + 2, sizeof(int64_t));
-    int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
-    int64_t* ord = (int64_t*)malloc(sizeof(int64_t) * (size_t)m);
-    uint8_t* alive = (uint8_t*)malloc((size_t)m);
-    for (int64_t e = 0; e < m; ++e) bin[S[e] + 1]++;
-    for (uint32_t s = 0; s <= smax; ++s) bin[s + 1] += bin[s];
-    {
-        int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * ((size_t)smax + 1));
-        for (uint32_t s = 0; s <= smax; ++s) fill[s] = bin[s];
-        for (int64_t e = 0; e < m; ++e) { pos[e] = fill[S[e]]++; ord[pos[e]] = e; }
-        free(fill);
+    if (m > INT32_MAX) return -1;
+    int32_t* col = col_in;
+    int32_t* eid = eid_in;
+    if (!consume) {
+        col = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * m));
+        eid = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * m));
+        if (!col || !eid) { free(col); free(eid); return -1; }
+        memcpy(col, col_in, sizeof(int32_t) * (size_t)(2 * m));
+        memcpy(eid, eid_in, sizeof(int32_t) * (size_t)(2 * m));
     }
-    for (int64_t e = 0; e < m; ++e) alive[e] = 1;
+    o7_edge* E = (o7_edge*)malloc(sizeof(o7_edge) * (size_t)m);
+    int32_t* ord = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+    int64_t* len = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));   /* stored entries */
+    int64_t* live = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));  /* live entries */
+    int64_t cap = 1024;
+    int32_t* hits = (int32_t*)malloc(sizeof(int32_t) * (size_t)cap * 2);          /* (f, g) pairs of e */
+    uint32_t smax = 0;
+    for (int64_t e = 0; e < m; ++e) if (sup_init[e] > smax) smax = sup_init[e];
+    int64_t* bin = (int64_t*)calloc((size_t)smax + 2, sizeof(int64_t));
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * ((size_t)smax + 1));
+    if (!E || !ord || !len || !live || !hits || !bin || !fill) {
+        free(E); free(ord); free(len); free(live); free(hits); free(bin); free(fill);
+        if (!consume) { free(col); free(eid); }
+        return -1;
+    }
+    for (int64_t x = 0; x < n; ++x) len[x] = live[x] = ptr[x + 1] - ptr[x];
+    for (int64_t e = 0; e < m; ++e) bin[sup_init[e] + 1]++;
+    for (uint32_t s = 0; s <= smax; ++s) bin[s + 1] += bin[s];
+    for (uint32_t s = 0; s <= smax; ++s) fill[s] = bin[s];
+    for (int64_t e = 0; e < m; ++e) {
+        E[e].s = sup_init[e];
+        E[e].pos = (int32_t)fill[sup_init[e]]++;
+        ord[E[e].pos] = (int32_t)e;
+    }
+    free(fill);
     int32_t kmax = 2;
     /* bin[s] = first position of bucket s among not-yet-processed slots */
     for (int64_t i = 0; i < m; ++i) {
         int64_t e = ord[i];
-        uint32_t se = S[e];
+        uint32_t se = E[e].s;
         tau[e] = (int32_t)se + 2;
         if (tau[e] > kmax) kmax = tau[e];
-        /* live triangles through e: w in N(a) ∩ N(b) with (a,w), (b,w) alive */
+        /* common neighbours w of a and b: (a,w), (b,w) */
         int32_t a = cu[e], b = cv[e];
-        int64_t p = ptr[a], p1 = ptr[a + 1], q = ptr[b], q1 = ptr[b + 1];
-        while (p < p1 && q < q1) {
-            if (col[p] < col[q]) ++p;
-            else if (col[p] > col[q]) ++q;
-            else {
-                int64_t f = eid[p], g = eid[q];
-                if (alive[f] && alive[g]) {
-                    int64_t fg[2] = {f, g};
-                    for (int t = 0; t < 2; ++t) {
-                        int64_t h = fg[t];
-                        if (S[h] > se) {
-                            /* move h to the front of its bucket, then shrink it by one */
-                            uint32_t sh = S[h];
-                            int64_t first = bin[sh];
-                            if (first < i + 1) first = i + 1;
-                            int64_t hw = ord[first];
-                            if (hw != h) {
-                                ord[pos[h]] = hw; pos[hw] = pos[h];
-                                ord[first] = h; pos[h] = first;
-                            }
-                            bin[sh] = first + 1;
-                            S[h] = sh - 1;
-                        }
+        int64_t p = ptr[a], p1 = ptr[a] + len[a], q = ptr[b], q1 = ptr[b] + len[b];
+        if (p1 - p > q1 - q) {                     /* p walks the shorter row */
+            int64_t t;
+            t = p; p = q; q = t; t = p1; p1 = q1; q1 = t;
+        }
+        int gallop = (q1 - q) >= O7_GALLOP * (p1 - p);
+        int64_t nh = 0;
+        for (; p < p1 && q < q1; ++p) {
+            if (gallop) {
+                q = gallop32(col, q, q1, col[p]);
+                if (q >= q1) break;
+            } else {
+                while (q < q1 && col[q] < col[p]) ++q;
+                if (q >= q1) break;
+            }
+            if (col[q] != col[p]) continue;
+            if (nh == cap) {
+                cap *= 2;
+                int32_t* nhits = (int32_t*)realloc(hits, sizeof(int32_t) * (size_t)cap * 2);
+                if (!nhits) { nh = -1; break; }
+                hits = nhits;
+            }
+            hits[2 * nh] = eid[p]; hits[2 * nh + 1] = eid[q];
+            __builtin_prefetch(&E[eid[p]]); __builtin_prefetch(&E[eid[q]]);
+            ++nh; ++q;
+        }
+        if (nh < 0) break;
+        /* live triangles (both other edges alive) cost each of them one unit */
+        for (int64_t j = 0; j < nh; ++j) {
+            int64_t f = hits[2 * j], g = hits[2 * j + 1];
+            if (E[f].pos < 0 || E[g].pos < 0) continue;
+            int64_t fg[2] = {f, g};
+            for (int t = 0; t < 2; ++t) {
+                int64_t h = fg[t];
+                if (E[h].s > se) {
+                    /* move h to the front of its bucket, then shrink it by one */
+                    uint32_t sh = E[h].s;
+                    int64_t first = bin[sh];
+                    if (first < i + 1) first = i + 1;
+                    int64_t hw = ord[first];
+                    if (hw != h) {
+                        ord[E[h].pos] = (int32_t)hw; E[hw].pos = E[h].pos;
+                        ord[first] = (int32_t)h; E[h].pos = (int32_t)first;
                     }
+                    bin[sh] = first + 1;
+                    E[h].s = sh - 1;
                 }
-                ++p; ++q;
             }
         }
-        alive[e] = 0;
+        E[e].pos = -1;                             /* removed */
         /* buckets below the next slot are exhausted */
         if (bin[se] < i + 1) bin[se] = i + 1;
+        /* drop dead entries from a row that is mostly dead */
+        int32_t ab[2] = {a, b};
+        for (int t = 0; t < 2; ++t) {
+            int32_t x = ab[t];
+            live[x]--;
+            if (len[x] > 2 * live[x] + 16) {
+                int64_t w = ptr[x];
+                for (int64_t r = ptr[x]; r < ptr[x] + len[x]; ++r)
+                    if (E[eid[r]].pos >= 0) { col[w] = col[r]; eid[w] = eid[r]; ++w; }
+                len[x] = w - ptr[x];
+            }
+        }
     }
+    int ok = 1;
+    for (int64_t e = 0; e < m; ++e) if (E[e].pos >= 0) { ok = 0; break; }   /* OOM mid-run */
     *kmax_out = kmax;
-    free(S); free(bin); free(pos); free(ord); free(alive);
-    return m;
+    free(E); free(bin); free(ord); free(len); free(live); free(hits);
+    if (!consume) { free(col); free(eid); }
+    return ok ? m : -1;
 }

@@ -1,0 +1,150 @@
+"""Expected values for the full-size configs C3, C4, C5, written ONLY by the CPU
+oracle (oracle/) from the seeded generator (gen/).  Nothing here imports or
+runs the CUDA path; the GPU parity tests (tests/test_parity_gpu.py) compare
+libgc's outputs with the files this script writes:
+
+    tests/golden/c3_expected.json   T (O-4), supports (O-3), k-truss masks for
+                                     k = 3..6 (O-5, Alg. 4 batch semantics) and
+                                     trussness (O-7), cross-checked: mask_k ==
+                                     (tau >= k) (reading A8)
+    tests/golden/c4_expected.json   T, supports, trussness / kmax (O-7), masks
+                                     for k = 3..6 derived as tau >= k
+    tests/golden/c5_expected.json   the same for C5
+
+Every per-edge array is stored as the SHA-256 of its canonical-order bytes
+(uint32 supports, int32 trussness, uint8 masks) plus its histogram, so a
+mismatch also shows where the counts differ.  O-3 vs O-4 is checked here
+(Σ support = 3 T, P4).  Phase times, thread counts and the CPU model are
+recorded: they are the full oracle runs the bench report quotes.
+
+    python scripts/make_golden.py C3 [C4 C5]    (C5: ~45 GB RAM, hours)
+
+Arrays are cached under exp/golden_cache/ (git- and gpurun-ignored) so a
+rerun resumes after the support pass.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import gen      # noqa: E402
+import oracle   # noqa: E402
+
+CACHE = os.path.join(ROOT, "exp", "golden_cache")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def log(*a):
+    print(time.strftime("%H:%M:%S"), *a, flush=True)
+
+
+def hist(a: np.ndarray) -> dict:
+    vals, cnt = np.unique(a, return_counts=True)
+    return {str(int(x)): int(c) for x, c in zip(vals, cnt)}
+
+
+def run(name: str, ktruss_batch: tuple = ()) -> dict:
+    os.makedirs(CACHE, exist_ok=True)
+    cfg = gen.CONFIGS[name]
+    times = {}
+    t = time.time()
+    u, v = cfg.generate()
+    nnz = int(u.size)
+    times["generate_s"] = time.time() - t
+    log(name, "generated", nnz)
+    t = time.time()
+    g = oracle.OracleGraph(u, v)
+    del u, v
+    times["canonicalize_adjacency_s"] = time.time() - t
+    log(name, "graph n", g.n, "m", g.m, f"{times['canonicalize_adjacency_s']:.1f}s")
+    out = {"_source": ("written by scripts/make_golden.py from oracle/ only (O-1..O-5, O-7; "
+                       "SURVEY.md §8(c)); per-edge arrays in canonical edge order (SURVEY §8(b))"),
+           "config": name, "desc": cfg.desc, "nnz": nnz, "n": g.n, "m": g.m,
+           "canonical_sha256": sha(np.stack([g.cu, g.cv], axis=1))}
+
+    sp = os.path.join(CACHE, f"{name}_support.npy")
+    if os.path.exists(sp):
+        sup = np.load(sp)
+        times["support_s"] = json.load(open(sp + ".json"))["support_s"]
+        log(name, "support from cache")
+    else:
+        t = time.time()
+        sup = g.support()                                   # O-3
+        times["support_s"] = time.time() - t
+        np.save(sp, sup)
+        json.dump({"support_s": times["support_s"]}, open(sp + ".json", "w"))
+        log(name, f"support {times['support_s']:.1f}s")
+    t = time.time()
+    T = g.triangle_count()                                  # O-4
+    times["triangle_count_s"] = time.time() - t
+    assert int(sup.astype(np.int64).sum()) == 3 * T, "O-3 / O-4 disagree (P4)"
+    log(name, "T", T, f"{times['triangle_count_s']:.1f}s")
+    out.update(triangles=T, support_sha256=sha(sup.astype(np.uint32)), support_max=int(sup.max(initial=0)),
+               support_zero=int((sup == 0).sum()))
+
+    masks = {}
+    for k in ktruss_batch:                                  # O-5, the definition
+        t = time.time()
+        alive, trace = g.ktruss(k)
+        times[f"ktruss{k}_s"] = time.time() - t
+        masks[k] = alive
+        out.setdefault("ktruss_rounds", {})[str(k)] = trace.tolist()
+        log(name, f"O-5 k={k}: {int(alive.sum())} edges, {trace.size} rounds, {times[f'ktruss{k}_s']:.1f}s")
+
+    t = time.time()
+    tau, kmax = g.truss_sequential(sup, consume=True)      # O-7 (uses the rows in place)
+    times["truss_sequential_s"] = time.time() - t
+    log(name, "O-7 kmax", kmax, f"{times['truss_sequential_s']:.1f}s")
+    np.save(os.path.join(CACHE, f"{name}_tau.npy"), tau)
+    for k, alive in masks.items():
+        assert np.array_equal(alive.astype(bool), tau >= k), f"O-5 k={k} != O-7 tau >= k (reading A8)"
+    out.update(kmax=kmax, trussness_sha256=sha(tau.astype(np.int32)), trussness_hist=hist(tau))
+    out["ktruss_size"] = {}
+    out["ktruss_sha256"] = {}
+    for k in sorted(set(range(3, 7)) | {kmax, kmax + 1}):
+        mk = (tau >= k).astype(np.uint8)
+        out["ktruss_size"][str(k)] = int(mk.sum())
+        out["ktruss_sha256"][str(k)] = sha(mk)
+    out["oracle_times"] = {**{k: round(v, 3) for k, v in times.items()},
+                           "threads": os.cpu_count(), "truss_sequential_threads": 1,
+                           "cpu": cpu_model(), "host": platform.node()}
+    return out
+
+
+def main(argv):
+    names = argv or ["C3"]
+    for name in names:
+        ks = (3, 4, 5, 6) if name == "C3" else ()
+        d = run(name, ks)
+        path = os.path.join(GOLDEN, f"{name.lower()}_expected.json")
+        with open(path, "w") as f:
+            json.dump(d, f, indent=1, sort_keys=True)
+            f.write("\n")
+        log("wrote", path)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

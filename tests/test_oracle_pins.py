@@ -178,7 +178,8 @@ def test_normalization_property():
 
 
 # --------------------------------------------------- paper worked examples --
-@pytest.mark.parametrize("fixture", ["fig1_diamond.json", "k4_ear.json", "pendant_triangle.json"])
+@pytest.mark.parametrize("fixture", ["fig1_diamond.json", "k4_ear.json", "pendant_triangle.json",
+                                     "hub_two_k4.json"])
 def test_golden_examples(fixture):
     d = json.load(open(os.path.join(GOLDEN, fixture)))
     g = oracle.OracleGraph(d["raw_u"], d["raw_v"])
@@ -569,3 +570,49 @@ def test_king_grid_configs_match_table2():
         cfg = gen.CONFIGS[name]
         assert cfg.n == 2 ** nn and cfg.n ** 2 == rows[nn][0]
         assert 2 * (cfg.n - 1) * (2 * cfg.n - 1) == rows[nn][1]
+
+
+# ------------------------------------------- skewed pairs (galloping branches) --
+@st.composite
+def hub_graphs(draw):
+    """A random core (n <= 16) plus a hub whose degree is >= 32x every core
+    degree: the hub joins a random subset of the core and enough outside
+    vertices, some of which are joined to each other and to the core, so
+    hub-core pairs take the oracle's binary-search branches (O-3, O-5, O-7)
+    while the hub's triangles die and live in every combination."""
+    n = draw(st.integers(3, 16))
+    pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
+    core = draw(st.lists(st.sampled_from(pairs), max_size=len(pairs), unique=True))
+    hub = n
+    joins = draw(st.lists(st.integers(0, n - 1), min_size=1, max_size=n, unique=True))
+    npend = 32 * n + draw(st.integers(0, 40))
+    first = n + 1
+    extra = draw(st.lists(st.tuples(st.integers(0, npend - 1), st.integers(0, npend - 1)), max_size=12))
+    cross = draw(st.lists(st.tuples(st.integers(0, npend - 1), st.integers(0, n - 1)), max_size=6))
+    u = [a for a, _ in core] + [hub] * len(joins) + [hub] * npend
+    v = [b for _, b in core] + joins + list(range(first, first + npend))
+    u += [first + a for a, _ in extra] + [first + a for a, _ in cross]
+    v += [first + b for _, b in extra] + [b for _, b in cross]
+    return np.array(u, np.int32), np.array(v, np.int32)
+
+
+@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(hub_graphs())
+def test_hypothesis_hub_graphs(raw):
+    """Degree ratios >= 32: supports = (A^2)(u,v), T =
+    trace(A^3)/6, k-trusses = networkx for k = 3..5, O-6 == O-7."""
+    u, v = raw
+    g = oracle.OracleGraph(u, v)
+    A = dense_adj(g)
+    A2 = A @ A
+    assert g.triangle_count() == int(np.trace(A2 @ A)) // 6
+    assert np.array_equal(g.support(), A2[g.cu, g.cv])
+    G = nx_graph(g)
+    idx = edge_index(g)
+    for k in (3, 4, 5):
+        want = {idx[(min(a, b), max(a, b))] for a, b in nx.k_truss(G, k).edges()}
+        alive, _ = g.ktruss(k)
+        assert set(np.flatnonzero(alive).tolist()) == want, k
+    tau, kmax = g.truss_decomposition()
+    tau2, kmax2 = g.truss_sequential()
+    assert np.array_equal(tau, tau2) and kmax == kmax2
