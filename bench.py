@@ -6,10 +6,12 @@
 
 One step = one pass of the whole hot path over the resident
 raw edge list of the workload: gc_build_csr (canonicalise, dedup, degrees,
-orient, task binning) + gc_ktruss_analysis(3): one support pass whose
+orient, task binning) + gc_ktruss_analysis(4): one support pass whose
 per-edge supports are written out, whose triangle total is the triangle
 count (the north star: "triangle counting sums this support"), and which
-seeds the k-truss peel to its fixed point.  The same results through the
+seeds the k-truss peel, run to its fixed point (k = 4 takes peel rounds;
+k = 3 needs none: a 3-truss is the edges with support >= 1 — its step is
+reported beside the headline as "k3_step").  The same results through the
 separate cold calls (gc_triangle_count + gc_edge_support + gc_ktruss) are
 timed after it and reported as "separate_calls".  Rate = m / step time with
 m the undirected deduplicated edge count (reading A14).  For N > 1 (torchrun) every rank holds the full graph, the intersection
@@ -46,7 +48,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="C4")
-    p.add_argument("--ktruss-k", type=int, default=3)
+    p.add_argument("--ktruss-k", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extra", action="store_true", help="skip the k = 4..6 trusses and the decomposition")
@@ -200,9 +202,18 @@ def cpu_baseline(cfg, u, v, sample):
     g.support_pairs(g.cu[idx], g.cv[idx])
     t_sup = time.perf_counter() - t1
     t_full = t_build + t_sup * g.m / max(S, 1)
-    return {"value": g.m / t_full, "unit": "edges/s", "cores": cores, "kind": "oracle",
-            "sample": f"{cfg.name}: oracle canonicalise+adjacency of the full graph ({t_build:.1f} s) + per-edge "
-                      f"support of {S} random edges ({t_sup:.1f} s), extrapolated to all m edges (TC+support only)"}
+    out = {"value": g.m / t_full, "unit": "edges/s", "cores": cores, "kind": "oracle",
+           "sample": f"{cfg.name}: oracle canonicalise+adjacency of the full graph ({t_build:.1f} s) + per-edge "
+                     f"support of {S} random edges ({t_sup:.1f} s), extrapolated to all m edges (TC+support only)"}
+    gpath = os.path.join(ROOT, "tests", "golden", f"{cfg.name.lower()}_expected.json")
+    if os.path.exists(gpath):
+        # the full oracle run of this config (scripts/make_golden.py, not this box): every phase in full
+        ot = json.load(open(gpath)).get("oracle_times", {})
+        full = ot.get("canonicalize_adjacency_s", 0) + ot.get("support_s", 0)
+        out["full_run"] = {**ot, "tc_support_edges_per_s": g.m / full if full else None,
+                           "note": "scripts/make_golden.py on the build container; truss_sequential is O-7, "
+                                   "one thread (tier-2 decomposition)"}
+    return out
 
 
 # --------------------------------------------------------------------- ours --
@@ -220,6 +231,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1708_06866_b200 import Context, init_distributed
+    from paper_1708_06866_b200.gc import GC_OPT_WORK_STATS
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -323,8 +335,30 @@ def main():
     sep_ms = timed(separate_step, args.steps)
     tck = float(np.mean(sep["tc_kernel_ms"]))
 
+    # ---- the k = 3 step (no peel rounds) beside the headline
+    def k3_step():
+        ctx.build_csr()
+        ctx.ktruss_analysis(3, sup_out, mask_out)
+
+    k3_ms = timed(k3_step, args.steps)
+
+    # ---- k-truss byte-model terms: one untimed pass of the
+    # same call with GC_OPT_WORK_STATS (identical work; counters only)
+    def work_terms(fn):
+        ctx.set_option(GC_OPT_WORK_STATS, 1)
+        try:
+            fn()
+            st_w = ctx.stats()
+        finally:
+            ctx.set_option(GC_OPT_WORK_STATS, 0)
+        return {"sum_min": st_w["peel_sum_min"], "decrements": st_w["peel_decrements"]}
+
+    work_k = work_terms(lambda: ctx.ktruss_analysis(k, sup_out, mask_out))
+
     # ---- deeper trusses and the decomposition on the same graph (reported, not the step)
     deeper = {}
+    work_decomp = None
+    decomp_ms = None
     if not args.no_extra:
         ctx.ktruss_analysis(4, sup_out, mask_out)          # first peel with rounds: row buffers allocated
         for kk in (4, 5, 6):
@@ -334,8 +368,11 @@ def main():
         tau_out = torch.empty(m, dtype=torch.int32, device="cuda")
         res = {}
         t = timed(lambda: res.update(kmax=ctx.truss_decomposition(tau_out)[1]), 1)
+        decomp_ms = t
         deeper.update({"decomposition_ms": t, "kmax": res.get("kmax"),
-                       "decomposition_rounds": ctx.stats()["peel_rounds"]})
+                       "decomposition_rounds": ctx.stats()["peel_rounds"],
+                       "decomposition_kernel_ms": ctx.stats()["decomp_ms"]})
+        work_decomp = work_terms(lambda: ctx.truss_decomposition(tau_out))
 
     # ---- roofline of the dominant kernel: the support intersection pass; TC pass beside it
     peak, peak_src = hbm_peak()
@@ -350,10 +387,14 @@ def main():
             ncu = {}
 
     def roof(kernel_ms, b_alg, key, label):
-        achieved = b_alg / (kernel_ms / 1e3) / 1e9 if kernel_ms > 0 else None
+        achieved = b_alg / (kernel_ms / 1e3) / 1e9 if kernel_ms and kernel_ms > 0 else None
+        traffic = ncu.get(key, {}).get("dram_bytes_per_launch")
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": ncu.get(key, {}).get("dram_bytes_per_launch"),
+                "traffic": traffic,
+                # DRAM bytes the kernel really moved (ncu) over the same time: the
+                # fraction of HBM bandwidth in use, beside the algorithmic one
+                "dram_frac": (traffic / (kernel_ms / 1e3) / 1e9 / peak) if traffic and kernel_ms else None,
                 "kernel": label, "algorithmic_bytes": b_alg, "kernel_ms": kernel_ms, "peak_source": peak_src}
 
     sup_ms = float(np.mean(phase["support_kernel_ms"]))
@@ -362,6 +403,27 @@ def main():
                     "the step's dominant kernel")
     roofline_tc = roof(tck, b_tc, "tc", "triangle-count intersection pass (k_tc_* class kernels, SUP=0; "
                                         "gc_triangle_count, measured in the separate-calls step)")
+
+    def b_ktruss(w, out_bytes):
+        # B_support + Σ_removed 4 min(d_ρ(u), d_ρ(v)) + 8 D + output
+        if not w or w["sum_min"] is None or w["sum_min"] < 0:
+            return None
+        return b_sup + 4 * w["sum_min"] + 8 * w["decrements"] + out_bytes
+
+    kt_ms = float(np.mean(phase["ktruss_ms"]))
+    bk = b_ktruss(work_k, m)
+    roofline_ktruss = roof(kt_ms, bk, "ktruss", f"gc_ktruss_analysis(k={k}) of the timed step: support pass + "
+                                               "peel to the fixed point (device time of the call)") if bk else None
+    if roofline_ktruss:
+        roofline_ktruss["terms"] = {**work_k, "b_support": b_sup}
+    roofline_decomposition = None
+    if work_decomp and decomp_ms:
+        bd = b_ktruss(work_decomp, 4 * m)
+        if bd:
+            dk = deeper.get("decomposition_kernel_ms") or decomp_ms
+            roofline_decomposition = roof(dk, bd, "decomposition", "gc_truss_decomposition: support pass + every "
+                                                                   "level's peel (device time of the call)")
+            roofline_decomposition["terms"] = {**work_decomp, "b_support": b_sup}
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -433,6 +495,13 @@ def main():
                        "parallelism": f"replicated graph, {world}-way balanced 1D intersection split"},
             "roofline": roofline,
             "roofline_tc": roofline_tc,
+            "roofline_ktruss": roofline_ktruss,
+            "roofline_decomposition": roofline_decomposition,
+            "tc_kernel_rate": {"value": m / (tck / 1e3), "unit": "edges/s", "kernel_ms": tck,
+                               "what": "m / triangle-count intersection pass (SURVEY A15's primary reading: "
+                                       "kernel time with the CSR built; the build is reported in phase_ms)"},
+            "k3_step": {"ms_per_step": k3_ms, "value": m / (k3_ms / 1e3), "unit": "edges/s",
+                        "step": "gc_build_csr + gc_ktruss_analysis(3) (the 3-truss needs no peel round)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -225,7 +225,8 @@ typedef enum gc_option {
                                  (default); 0: always its hash table (testing) */
     GC_OPT_SUP_SKIP = 7,      /* timing diagnostics only (wrong supports when nonzero):
                                  mask of support roles to skip, 1 (u,w), 2 (v,w),
-                                 4 (u,v); default 0 */
+                                 4 (u,v); default 0.  A nonzero value is refused with
+                                 GC_ERR_INVALID unless the environment has GC_DIAG=1 */
     GC_OPT_PEEL_PART = 8,     /* 1: use the partitioned k-truss peeler (removed-edge
                                  bitmap per round, owner-only decrements; the multi-GPU
                                  path) even on a single rank (testing); it is always
@@ -236,7 +237,9 @@ typedef enum gc_option {
     GC_OPT_COMPACT = 10,      /* peeler: drop dead entries from the adjacency rows each
                                  time the live edge count falls to (value-1)/value of the
                                  last compaction during gc_truss_decomposition (default 5,
-                                 i.e. 4/5; a single k-truss uses min(value, 2)); 0 or 1: never */
+                                 i.e. 4/5; a single k-truss uses min(value, 2)); 0 or 1: never.
+                                 (Before round 2 a value v meant "at 1/v"; 2 means the same
+                                 in both readings, 3 now means 2/3 instead of 1/3.) */
     GC_OPT_OVERLAP = 13,      /* 1: the warp-task intersection kernels run on a library
                                  side stream that overlaps the block-task kernels and is
                                  joined before the call returns (default); 0: one stream */
@@ -247,6 +250,10 @@ typedef enum gc_option {
                                  whose row is staged once per group as a shared-memory bitmap */
     GC_OPT_GROUP_HEAVY = 14,  /* ... heavy = shorter live row at least this long (default
                                  1024); lighter edges keep the per-edge search */
+    GC_OPT_WORK_STATS = 15,   /* 1: the single-rank peeler also counts the k-truss byte
+                                 model's terms (gc_stats peel_sum_min,
+                                 peel_decrements) at the cost of a few small kernels per
+                                 round (default 0; measurement) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 
@@ -277,6 +284,10 @@ typedef struct gc_stats {
     int64_t tasks[4];         /* intersection tasks per kernel class (last build) */
     int64_t aux[8];           /* heads with d+ > 256 by rank span of N+ (<=2^17, 2^18,
                                  2^19, more): counts [0..3], in-degree weighted [4..7] */
+    int64_t peel_sum_min;     /* GC_OPT_WORK_STATS, last peel: sum over rounds, over frontier
+                                 edges (a,b) with support > 0, of min(d(a), d(b)) (alive
+                                 degrees at the round start); -1 when not counted */
+    int64_t peel_decrements;  /* ... support decrements D applied to surviving edges; -1 */
 } gc_stats;
 int gc_get_stats(const gc_ctx* ctx, gc_stats* out);
 int gc_reset_stats(gc_ctx* ctx);

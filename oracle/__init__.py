@@ -43,10 +43,10 @@ def _lib():
         L.or_triangle_count.argtypes = [i64p, i32p, ctypes.c_int64, i32p, i32p, ctypes.c_int]
         L.or_triangle_count.restype = ctypes.c_uint64
         L.or_ktruss.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p, i32p,
-                                ctypes.c_int32, u8p, i64p, ctypes.c_int64, ctypes.c_int]
+                                ctypes.c_int32, u8p, i64p, ctypes.c_int64, ctypes.c_int, i64p]
         L.or_ktruss.restype = ctypes.c_int64
         L.or_truss_decomposition.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p,
-                                             i32p, i32p, i32p, ctypes.c_int]
+                                             i32p, i32p, i32p, ctypes.c_int, i64p]
         L.or_truss_decomposition.restype = ctypes.c_int64
         L.or_truss_sequential.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p,
                                           i32p, u32p, i32p, i32p, ctypes.c_int]
@@ -111,23 +111,33 @@ class OracleGraph:
                                             _p(self.cu, i32p), _p(self.cv, i32p), self.nthreads))
 
     # O-5
-    def ktruss(self, k: int, trace_cap: int = 1 << 16):
+    def ktruss(self, k: int, trace_cap: int = 1 << 16, work: bool = False):
+        """(alive mask, |x| per round); work=True adds {"sum_min", "decrements"}:
+        the k-truss byte model's terms over the batch rounds (oracle.c peel_batch)."""
         alive = np.zeros(max(self.m, 1), dtype=np.uint8)
         trace = np.zeros(trace_cap, dtype=np.int64)
+        w = np.zeros(2, dtype=np.int64)
         r = _lib().or_ktruss(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p), _p(self.ptr, i64p),
                              _p(self.col, i32p), _p(self.eid, i32p), int(k), _p(alive, u8p),
-                             _p(trace, i64p), trace_cap, self.nthreads)
+                             _p(trace, i64p), trace_cap, self.nthreads, _p(w, i64p) if work else None)
         if r < 0:
             raise ValueError("k must be >= 2")
-        return alive[: self.m].copy(), trace[: min(r, trace_cap)].copy()
+        out = (alive[: self.m].copy(), trace[: min(r, trace_cap)].copy())
+        if work:
+            return out + ({"sum_min": int(w[0]), "decrements": int(w[1])},)
+        return out
 
     # O-6
-    def truss_decomposition(self):
+    def truss_decomposition(self, work: bool = False):
         tau = np.zeros(max(self.m, 1), dtype=np.int32)
         kmax = ctypes.c_int32(0)
+        w = np.zeros(2, dtype=np.int64)
         _lib().or_truss_decomposition(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p),
                                       _p(self.ptr, i64p), _p(self.col, i32p), _p(self.eid, i32p),
-                                      _p(tau, i32p), ctypes.byref(kmax), self.nthreads)
+                                      _p(tau, i32p), ctypes.byref(kmax), self.nthreads,
+                                      _p(w, i64p) if work else None)
+        if work:
+            return tau[: self.m].copy(), int(kmax.value), {"sum_min": int(w[0]), "decrements": int(w[1])}
         return tau[: self.m].copy(), int(kmax.value)
 
     # O-7

@@ -266,23 +266,48 @@ static void rs_range(void* c, int64_t e0, int64_t e1, int t) {
  * (s = (R==2)·1 with R = E·A of the alive graph), then
  * removes x = {alive e : s(e) < k-2} as a batch.
  * removed_level (optional): set to `level_tag` for edges removed here.
- * trace (optional, cap trace_cap): |x| per round.  Returns #rounds with
- * non-empty x. */
+ * trace (optional, cap trace_cap): |x| per round.
+ * work (optional, 2 entries, accumulated): the k-truss byte model's terms
+ * (SURVEY §8(d)): work[0] += Σ over rounds, over e = (a,b) in x with
+ * s(e) > 0, of min(d(a), d(b)), d = alive degree at the round start;
+ * work[1] += D, the support decrements: Σ over rounds of the drop of s on the
+ * edges that stay (s at this round's recompute minus s at the next).
+ * Returns #rounds with non-empty x. */
 static int64_t peel_batch(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
                           const int64_t* ptr, const int32_t* col, const int32_t* eid,
                           int32_t k, uint8_t* alive, uint32_t* s,
                           int32_t* removed_level, int32_t level_tag,
-                          int64_t* trace, int64_t trace_cap, int64_t trace_base, int nthreads) {
-    (void)n;
+                          int64_t* trace, int64_t trace_cap, int64_t trace_base, int nthreads,
+                          int64_t* work) {
     int64_t rounds = 0;
+    uint32_t* prev = NULL;
+    int64_t* d = NULL;
+    if (work) {
+        prev = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
+        d = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    }
+    int have_prev = 0;
     for (;;) {
         rs_ctx C = {ptr, col, eid, cu, cv, alive, s};
         parallel_for(m, nthreads, rs_range, &C);
+        if (work && have_prev)
+            for (int64_t e = 0; e < m; ++e)
+                if (alive[e]) work[1] += (int64_t)prev[e] - (int64_t)s[e];
         int64_t nx = 0;
+        if (work) {
+            for (int64_t x = 0; x < n; ++x) d[x] = 0;
+            for (int64_t e = 0; e < m; ++e)
+                if (alive[e]) { d[cu[e]]++; d[cv[e]]++; }
+        }
         /* x is decided for all edges before any is removed (batch) */
         for (int64_t e = 0; e < m; ++e)
-            if (alive[e] && (int64_t)s[e] < (int64_t)k - 2) { s[e] = 0xFFFFFFFFu; ++nx; }
+            if (alive[e] && (int64_t)s[e] < (int64_t)k - 2) {
+                if (work && s[e] > 0) work[0] += d[cu[e]] < d[cv[e]] ? d[cu[e]] : d[cv[e]];
+                s[e] = 0xFFFFFFFFu;
+                ++nx;
+            }
         if (nx == 0) break;
+        if (work) { memcpy(prev, s, sizeof(uint32_t) * (size_t)m); have_prev = 1; }
         for (int64_t e = 0; e < m; ++e)
             if (alive[e] && s[e] == 0xFFFFFFFFu) {
                 alive[e] = 0;
@@ -291,20 +316,25 @@ static int64_t peel_batch(int64_t n, int64_t m, const int32_t* cu, const int32_t
         if (trace && trace_base + rounds < trace_cap) trace[trace_base + rounds] = nx;
         ++rounds;
     }
+    free(prev);
+    free(d);
     return rounds;
 }
 
 /* ------------------------------------------------------------------ O-5 --
  * Maximal k-truss (reading A2), k >= 2.  alive_out: m (1 = kept).
- * trace: |x| per round (may be NULL).  Returns the number of rounds, or -1
- * for k < 2 (domain error). */
+ * trace: |x| per round (may be NULL).  work: see peel_batch (may be NULL).
+ * Returns the number of rounds, or -1 for k < 2 (domain error). */
 int64_t or_ktruss(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
                   const int64_t* ptr, const int32_t* col, const int32_t* eid,
-                  int32_t k, uint8_t* alive_out, int64_t* trace, int64_t trace_cap, int nthreads) {
+                  int32_t k, uint8_t* alive_out, int64_t* trace, int64_t trace_cap, int nthreads,
+                  int64_t* work) {
     if (k < 2) return -1;
     for (int64_t e = 0; e < m; ++e) alive_out[e] = 1;
     uint32_t* s = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
-    int64_t r = peel_batch(n, m, cu, cv, ptr, col, eid, k, alive_out, s, NULL, 0, trace, trace_cap, 0, nthreads);
+    if (work) work[0] = work[1] = 0;
+    int64_t r = peel_batch(n, m, cu, cv, ptr, col, eid, k, alive_out, s, NULL, 0, trace, trace_cap, 0, nthreads,
+                           work);
     free(s);
     return r;
 }
@@ -313,17 +343,19 @@ int64_t or_ktruss(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
  * Truss decomposition: run the k-truss with k = 3 on the full
  * graph, then pass the result to k+1, until empty.  tau(e) = k-1 for edges
  * removed at level k (so every edge has tau >= 2).  kmax = max tau, 0 when
- * m == 0 (reading A7).  Returns total rounds. */
+ * m == 0 (reading A7).  work: see peel_batch, summed over the levels (may
+ * be NULL).  Returns total rounds. */
 int64_t or_truss_decomposition(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv,
                                const int64_t* ptr, const int32_t* col, const int32_t* eid,
-                               int32_t* tau, int32_t* kmax_out, int nthreads) {
+                               int32_t* tau, int32_t* kmax_out, int nthreads, int64_t* work) {
     uint8_t* alive = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
     uint32_t* s = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
     for (int64_t e = 0; e < m; ++e) { alive[e] = 1; tau[e] = 2; }
     int64_t left = m, rounds = 0;
     int32_t kmax = 0;
+    if (work) work[0] = work[1] = 0;
     for (int32_t k = 3; left > 0; ++k) {
-        rounds += peel_batch(n, m, cu, cv, ptr, col, eid, k, alive, s, tau, k - 1, NULL, 0, 0, nthreads);
+        rounds += peel_batch(n, m, cu, cv, ptr, col, eid, k, alive, s, tau, k - 1, NULL, 0, 0, nthreads, work);
         left = 0;
         for (int64_t e = 0; e < m; ++e) left += alive[e];
     }

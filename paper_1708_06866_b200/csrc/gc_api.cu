@@ -35,12 +35,14 @@ int ensure(gc_ctx* c, Buf& b, size_t bytes) {
         b.cap = 0;
     }
     size_t want = bytes + bytes / 8;  // slack so growing configs do not thrash
-    cudaError_t e = cudaMallocAsync(&b.p, want, c->stream);
+    cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&b.p, want, c->pool, c->stream)
+                            : cudaMallocAsync(&b.p, want, c->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         b.p = nullptr;
         // retry without slack
-        e = cudaMallocAsync(&b.p, bytes, c->stream);
+        e = c->pool ? cudaMallocFromPoolAsync(&b.p, bytes, c->pool, c->stream)
+                    : cudaMallocAsync(&b.p, bytes, c->stream);
         if (e != cudaSuccess) {
             cudaGetLastError();
             b.p = nullptr;
@@ -172,6 +174,11 @@ static int check_ctx(const gc_ctx* c) {
 
 static thread_local std::string g_create_err;
 
+static bool diag_enabled() {
+    const char* e = getenv("GC_DIAG");
+    return e && e[0] == '1';
+}
+
 extern "C" {
 
 int gc_create(gc_ctx** out, int device, void* cuda_stream) {
@@ -203,11 +210,20 @@ int gc_create(gc_ctx** out, int device, void* cuda_stream) {
         }
         c->own_stream = true;
     }
-    // keep freed pool memory cached: steady-state steps then allocate nothing
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // a library-owned pool that keeps freed memory cached (steady-state steps
+    // then allocate nothing); the device's default pool is left untouched and
+    // everything this pool holds is returned by gc_destroy
+    {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        if (cudaMemPoolCreate(&c->pool, &props) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            c->pool = nullptr;      // fall back to the default pool's stream-ordered allocator
+        }
     }
     for (auto& ev : c->ev) cudaEventCreate(&ev);
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -230,9 +246,11 @@ int gc_destroy(gc_ctx* c) {
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->front_a,
-                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist};
+                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist,
+                        &c->vdeg, &c->zlist};
     for (auto* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
+    if (c->pool) cudaMemPoolDestroy(c->pool);   // returns the cached blocks to the device
     nccl_destroy(c);
     if (c->hpin) cudaFreeHost(c->hpin);
     for (auto& ev : c->ev)
@@ -513,6 +531,10 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
             }
             return GC_OK;
         case GC_OPT_SUP_SKIP:
+            // diagnostics only: skipped roles give wrong supports, so the option
+            // is refused unless the process opted in with GC_DIAG=1
+            if (value != 0 && !diag_enabled())
+                return fail(c, GC_ERR_INVALID, "GC_OPT_SUP_SKIP is a timing diagnostic (wrong supports); set GC_DIAG=1 to allow it");
             if (value < 0 || value > 7) return fail(c, GC_ERR_INVALID, "support skip mask must be 0..7");
             c->sup_skip = (int)value;
             return GC_OK;
@@ -537,6 +559,9 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
             return GC_OK;
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;
+            return GC_OK;
+        case GC_OPT_WORK_STATS:
+            c->work_stats = value ? 1 : 0;
             return GC_OK;
         case GC_OPT_TIMING:
             c->timing = value ? 1 : 0;

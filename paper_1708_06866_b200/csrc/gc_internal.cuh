@@ -56,6 +56,7 @@ struct Buf {
 
 struct gc_ctx {
     int device = 0;
+    cudaMemPool_t pool = nullptr;    // library-owned stream-ordered pool (release threshold: keep everything)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t side = nullptr;     // library-owned side stream (warp-task classes overlap the block kernels)
@@ -160,6 +161,9 @@ struct gc_ctx {
     gcx::Buf nbits;     // uint32 next-round bitmap (each owner sets bits in its slice)
     gcx::Buf sup_parts; // uint32[P*m] per-virtual-rank supports (loopback partitions only)
     int peel_part = 0;  // 1: partitioned (bitmap) peeler even on one rank (GC_OPT_PEEL_PART)
+    int work_stats = 0; // GC_OPT_WORK_STATS: count the k-truss byte model's terms while peeling
+    gcx::Buf vdeg;      // int32[n] alive degree per vertex (rank space; work stats only)
+    gcx::Buf zlist;     // int32[m] edges removed at a level scan with S = 0 (work stats only)
 
     // pinned host scratch
     void* hpin = nullptr;

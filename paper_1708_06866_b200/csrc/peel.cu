@@ -197,7 +197,8 @@ __global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restr
                                 const int32_t* __restrict__ list, int64_t len, uint32_t thr,
                                 int32_t round, int32_t* __restrict__ front,
                                 int* __restrict__ count, int32_t* __restrict__ tau, int32_t level,
-                                unsigned long long* __restrict__ zero_removed, uint32_t* __restrict__ min_rest) {
+                                unsigned long long* __restrict__ zero_removed, uint32_t* __restrict__ min_rest,
+                                int32_t* __restrict__ zlist, int* __restrict__ zcount) {
     const int lane = threadIdx.x & 31;
     unsigned zeros = 0;
     uint32_t rest = 0xFFFFFFFFu;   // min S over the alive edges left out of the frontier
@@ -209,6 +210,7 @@ __global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restr
             if (se == 0 && thr > 0) {
                 alive[e] = 0;
                 if (tau) tau[e] = level;
+                if (zlist) zlist[atomicAdd(zcount, 1)] = (int32_t)e;   // work stats only
                 ++zeros;
             } else {
                 in = se < thr;
@@ -699,6 +701,50 @@ __global__ void k_mask_from_support(const uint32_t* __restrict__ S, int64_t m, u
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(kept, (unsigned long long)c);
 }
 
+// ---- k-truss byte-model terms (GC_OPT_WORK_STATS)
+// alive degree of every vertex at the peel start (every edge alive)
+__global__ void k_vdeg_init(const int64_t* __restrict__ dag_ptr, const int64_t* __restrict__ in_ptr, int64_t n,
+                            int32_t* __restrict__ vdeg) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+        vdeg[x] = (int32_t)((dag_ptr[x + 1] - dag_ptr[x]) + (in_ptr[x + 1] - in_ptr[x]));
+}
+
+// acc += sum over the round's frontier edges e = (a,b) with S(e) > 0 of
+// min(vdeg[a], vdeg[b]) (degrees at the round start)
+__global__ void k_round_summin(const int32_t* __restrict__ front, const int* __restrict__ nfront_dev,
+                               const uint32_t* __restrict__ S, const int32_t* __restrict__ dag_src,
+                               const int32_t* __restrict__ dag_col, const int32_t* __restrict__ vdeg,
+                               unsigned long long* __restrict__ acc) {
+    const int nf = *nfront_dev;
+    unsigned long long sum = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+        const int e = front[i];
+        if (S[e] > 0) sum += (unsigned long long)min(vdeg[dag_src[e]], vdeg[dag_col[e]]);
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
+}
+
+// the removed edges leave their endpoints' alive degrees
+__global__ void k_round_vdeg(const int32_t* __restrict__ list, const int* __restrict__ n_dev,
+                             const int32_t* __restrict__ dag_src, const int32_t* __restrict__ dag_col,
+                             int32_t* __restrict__ vdeg) {
+    const int nl = *n_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) {
+        const int e = list[i];
+        atomicSub(vdeg + dag_src[e], 1);
+        atomicSub(vdeg + dag_col[e], 1);
+    }
+}
+
+__global__ void k_sum_u32(const uint32_t* __restrict__ a, int64_t m, unsigned long long* __restrict__ acc) {
+    unsigned long long sum = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        sum += a[i];
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, sum);
+}
+
 
 }  // namespace
 
@@ -856,6 +902,20 @@ static int peel_round_grouped(gc_ctx* c, const int32_t* front, int nf, const Pol
     return GC_OK;
 }
 
+// Work stats (GC_OPT_WORK_STATS): the edges of `gone` (count on the device)
+// leave the alive degrees, then the next round's frontier `next` adds its
+// min-degree term (either list may be null).
+static int work_round(gc_ctx* c, const int32_t* next, const int* next_n, const int32_t* gone, const int* gone_n) {
+    if (gone)
+        GC_LAUNCH(c, k_round_vdeg, 148 * 4, kThreads, 0, gone, gone_n, c->dag_src.as<int32_t>(),
+                  c->dag_col.as<int32_t>(), c->vdeg.as<int32_t>());
+    if (next)
+        GC_LAUNCH(c, k_round_summin, 148 * 4, kThreads, 0, next, next_n, c->sup.as<uint32_t>(),
+                  c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(), c->vdeg.as<int32_t>(),
+                  reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 672));
+    return GC_OK;
+}
+
 // Peel at threshold thr = k - 2 starting from the current alive set / S.
 // level >= 0: write tau = level for removed edges.  Returns removed count.
 #ifndef GC_BATCH_MAX_FRONT
@@ -891,9 +951,19 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
     uint32_t* min_rest = reinterpret_cast<uint32_t*>(c->scal.as<char>() + 320);
     GC_CUDA(c, cudaMemsetAsync(zrem, 0, 8, c->stream));
     GC_CUDA(c, cudaMemsetAsync(min_rest, 0xFF, 4, c->stream));
+    const bool ws = c->work_stats != 0;
+    int* zc = reinterpret_cast<int*>(c->scal.as<char>() + 688);
+    if (ws) GC_CUDA(c, cudaMemsetAsync(zc, 0, sizeof(int), c->stream));
     GC_LAUNCH(c, k_frontier_scan, grid_for(len), kThreads, 0, c->sup.as<uint32_t>(), c->alive.as<uint8_t>(), list,
               len, thr, *round, c->front_a.as<int32_t>(), cnt,
-              level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem, min_rest);
+              level >= 0 ? c->tau.as<int32_t>() : nullptr, level, zrem, min_rest,
+              ws ? c->zlist.as<int32_t>() : nullptr, zc);
+    if (ws) {
+        // round 1's X = the scan's frontier plus the zero-support edges it
+        // removed on the spot: its term uses the degrees before either leaves
+        GC_TRY(work_round(c, c->front_a.as<int32_t>(), cnt, nullptr, nullptr));
+        GC_TRY(work_round(c, nullptr, nullptr, c->zlist.as<int32_t>(), zc));
+    }
     GC_TRY(record(c, 11));
     GC_TRY(read_small(c, h, cnt, sizeof(int)));
     GC_TRY(read_small(c, h + 2, zrem, 8));
@@ -933,6 +1003,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             GC_TRY(peel_round_grouped(c, lists[cur], nf, pol));
             GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
                       level >= 0 ? c->tau.as<int32_t>() : nullptr, level, acc);
+            if (ws) GC_TRY(work_round(c, lists[nxt], counts[nxt], lists[cur], counts[cur]));
             GC_TRY(record(c, 9));
             ++*round;
             cur = nxt;
@@ -960,6 +1031,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             GC_TRY(launch_peel(c, 148 * 8, A, pol, r == 0 ? (int64_t)nf : 0));   // later rounds of a batch are small
             GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
                       level >= 0 ? c->tau.as<int32_t>() : nullptr, level, acc);
+            if (ws) GC_TRY(work_round(c, lists[nxt], counts[nxt], lists[cur], counts[cur]));
             ++*round;
             cur = nxt;
         }
@@ -1067,6 +1139,15 @@ static int peel_setup(gc_ctx* c) {
     c->stats.peel_rounds = 0;
     c->stats.compactions = 0;
     c->stats.peel_kernel_ms = c->stats.scan_ms = c->stats.compact_ms = 0;
+    c->stats.peel_sum_min = c->stats.peel_decrements = -1;
+    if (c->work_stats) {
+        GC_TRY(ensure(c, c->vdeg, (size_t)c->n * 4));
+        GC_TRY(ensure(c, c->zlist, (size_t)m * 4));
+        GC_CUDA(c, cudaMemsetAsync(c->scal.as<char>() + 672, 0, 16, c->stream));
+        if (c->n > 0)
+            GC_LAUNCH(c, k_vdeg_init, grid_for(c->n), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(),
+                      c->n, c->vdeg.as<int32_t>());
+    }
     const int P = peel_parts(c);
     if (P > 0) {
         const int64_t W = part_words(c, P);
@@ -1088,6 +1169,33 @@ static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int6
     if (next_thr) *next_thr = 0;
     if (peel_parts(c) > 0) return peel_level_part(c, thr, level, removed);
     return peel_level(c, thr, level, round, removed, next_thr);
+}
+
+// Work stats of the finished peel: Σ min-degree from its accumulator, and
+// D = 3T - Σ S(e) over every edge (a frontier edge's S freezes when it joins
+// X, a survivor's ends at its support inside the truss; each decrement took
+// one unit from 3T).  Not counted by the partitioned peeler (-1).
+static int work_collect(gc_ctx* c, bool peeled) {
+    if (!c->work_stats) return GC_OK;
+    if (!peeled) {
+        c->stats.peel_sum_min = c->stats.peel_decrements = 0;
+        return GC_OK;
+    }
+    if (peel_parts(c) > 0) {
+        c->stats.peel_sum_min = c->stats.peel_decrements = -1;
+        return GC_OK;
+    }
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 680);
+    GC_CUDA(c, cudaMemsetAsync(tot, 0, 8, c->stream));
+    if (c->m > 0) GC_LAUNCH(c, k_sum_u32, grid_for(c->m), kThreads, 0, c->sup.as<uint32_t>(), c->m, tot);
+    char* h = static_cast<char*>(c->hpin) + 768;
+    GC_TRY(read_small(c, h, c->scal.as<char>() + 672, 16));
+    GC_TRY(read_small(c, h + 16, support_hits(c), 8));
+    GC_TRY(sync(c));
+    const uint64_t* v = reinterpret_cast<const uint64_t*>(h);
+    c->stats.peel_sum_min = (int64_t)v[0];
+    c->stats.peel_decrements = 3 * (int64_t)v[2] - (int64_t)v[1];
+    return GC_OK;
 }
 
 int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
@@ -1116,6 +1224,7 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
         // {e : S(e) >= k - 2} straight from the support pass (same on every
         // rank: no collective).
         c->stats.peel_rounds = 0;
+        GC_TRY(work_collect(c, false));
         if ((alive_out || m_alive) && m > 0) {
             GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
             GC_TRY(ensure(c, c->alive, (size_t)m));
@@ -1140,6 +1249,7 @@ int ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support
             int32_t round = 0;
             GC_TRY(peel_any(c, (uint32_t)(k - 2), -1, &round, &removed));
         }
+        GC_TRY(work_collect(c, m > 0 && k > 2));
         if (alive_out && m > 0) {
             GC_TRY(ensure(c, c->out_tmp2, (size_t)m));
             if (support_out && c->stats.peel_rounds == 0) {
@@ -1194,6 +1304,7 @@ int truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
         // equal the current one: no trussness value to assign)
         if (next_thr > (uint32_t)(k - 1)) k = (int32_t)next_thr + 1;
     }
+    GC_TRY(work_collect(c, m > 0));
     *kmax = (m > 0) ? last : 0;
     GC_TRY(ensure(c, c->out_tmp, (size_t)m * 4));
     if (m > 0)

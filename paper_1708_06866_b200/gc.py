@@ -43,6 +43,7 @@ GC_OPT_COMPACT = 10
 GC_OPT_GROUP_PEEL = 12
 GC_OPT_GROUP_HEAVY = 14
 GC_OPT_OVERLAP = 13
+GC_OPT_WORK_STATS = 15
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -66,6 +67,7 @@ class gc_stats(ctypes.Structure):
         ("q_out", ctypes.c_int64), ("q_in", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
         ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),
         ("aux", ctypes.c_int64 * 8),
+        ("peel_sum_min", ctypes.c_int64), ("peel_decrements", ctypes.c_int64),
     ]
 
 

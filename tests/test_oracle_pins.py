@@ -616,3 +616,70 @@ def test_hypothesis_hub_graphs(raw):
     tau, kmax = g.truss_decomposition()
     tau2, kmax2 = g.truss_sequential()
     assert np.array_equal(tau, tau2) and kmax == kmax2
+
+
+# ------------------------------------------ k-truss byte-model terms (§8(d)) --
+def _batch_replay_work(edges, k):
+    """Plain-Python replay of Alg. 4's batch rounds on an edge set:
+    sum over rounds of min(d(a), d(b)) for x-edges with support > 0 (alive
+    degrees at the round start) and D = the support lost by edges that stay."""
+    alive = set(edges)
+    sum_min = dec = 0
+    prev = None
+    while True:
+        nb = {}
+        for a, b in alive:
+            nb.setdefault(a, set()).add(b)
+            nb.setdefault(b, set()).add(a)
+        s = {e: len(nb[e[0]] & nb[e[1]]) for e in alive}
+        if prev is not None:
+            dec += sum(prev[e] - s[e] for e in alive)
+        x = {e for e in alive if s[e] < k - 2}
+        if not x:
+            return sum_min, dec
+        sum_min += sum(min(len(nb[a]), len(nb[b])) for a, b in x if s[(a, b)] > 0)
+        prev = s
+        alive -= x
+
+
+def test_ktruss_work_terms_fixtures():
+    """Hand-derived (DESIGN.md §7 "k-truss roofline"): K4+ear at k = 4: round 1
+    removes (0,4), (1,4), min degrees 2 + 2, triangle (0,1,4) costs (0,1) one
+    unit; the hub fixture at k = 4: (w1,H), (w2,H) with min degree 4 each, the
+    two hub triangles cost 2 units each; the decompositions add every later
+    level's rounds; K_n at k = n+1: every edge in round 1, min degree n-1, no
+    survivor to decrement."""
+    d = json.load(open(os.path.join(GOLDEN, "k4_ear.json")))
+    g = oracle.OracleGraph(d["raw_u"], d["raw_v"])
+    assert g.ktruss(4, work=True)[2] == {"sum_min": 4, "decrements": 1}
+    assert g.truss_decomposition(work=True)[2] == {"sum_min": 4 + 6 * 3, "decrements": 1}
+    d = json.load(open(os.path.join(GOLDEN, "hub_two_k4.json")))
+    g = oracle.OracleGraph(d["raw_u"], d["raw_v"])
+    assert g.ktruss(4, work=True)[2] == {"sum_min": 8, "decrements": 4}
+    assert g.truss_decomposition(work=True)[2] == {"sum_min": 3 + 3 + 12 * 3, "decrements": 4}
+    for n in (4, 7, 12):
+        u, v = zip(*itertools.combinations(range(n), 2))
+        g = oracle.OracleGraph(list(u), list(v))
+        assert g.ktruss(n + 1, work=True)[2] == {"sum_min": math.comb(n, 2) * (n - 1), "decrements": 0}
+        assert g.ktruss(n, work=True)[2] == {"sum_min": 0, "decrements": 0}
+
+
+def test_ktruss_work_terms_bruteforce():
+    rng = np.random.default_rng(12)
+    graphs = [oracle.OracleGraph(*random_simple_graph(int(rng.integers(5, 40)), float(rng.uniform(0.1, 0.6)), rng))
+              for _ in range(15)]
+    graphs.append(oracle.OracleGraph(*gen.rmat(7, 8, seed=12)))
+    for g in graphs:
+        edges = list(zip(g.cu.tolist(), g.cv.tolist()))
+        tot = [0, 0]
+        for k in range(3, 9):
+            w = g.ktruss(k, work=True)[2]
+            assert (w["sum_min"], w["decrements"]) == _batch_replay_work(edges, k), k
+        # decomposition: k = 3, 4, ... each from the previous survivors (P:299-302)
+        tau, kmax, wd = g.truss_decomposition(work=True)
+        for k in range(3, kmax + 2):
+            surv = [e for e, t in zip(edges, tau.tolist()) if t >= k - 1]
+            sm, dc = _batch_replay_work(surv, k)
+            tot[0] += sm
+            tot[1] += dc
+        assert (wd["sum_min"], wd["decrements"]) == tuple(tot)

@@ -756,3 +756,32 @@ def test_errors(ctx, gcmod):
         with pytest.raises(gcmod.GcError) as e:
             c2.ktruss_analysis_async(1, np.empty(2, np.uint32), np.empty(2, np.uint8))
         assert e.value.code == gcmod.GC_ERR_INVALID
+
+
+# ------------------------------------------- k-truss byte-model terms (§8(d)) --
+def test_work_stats_match_oracle_replay(gcmod):
+    """GC_OPT_WORK_STATS: the peeler's Σ min(d(a), d(b)) over frontier edges
+    with support > 0 and its decrement count D equal the oracle's batch
+    replay (O-5 / O-6 with work=True) for single k-trusses and whole
+    decompositions — the terms bench.py's k-truss roofline is built from."""
+    cases = [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=71)]
+    for f in ("k4_ear.json", "hub_two_k4.json"):
+        d = json.load(open(os.path.join(GOLDEN, f)))
+        cases.append((np.array(d["raw_u"], np.int32), np.array(d["raw_v"], np.int32)))
+    for u, v in cases:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            c.set_option(gcmod.GC_OPT_WORK_STATS, 1)
+            c.load_edges(u, v)
+            c.build_csr()
+            for k in (3, 4, 5, 7):
+                want_mask, _, w = g.ktruss(k, work=True)
+                T, _, mask, _ = c.ktruss_analysis(k)
+                st = c.stats()
+                assert np.array_equal(mask, want_mask), k
+                assert (st["peel_sum_min"], st["peel_decrements"]) == (w["sum_min"], w["decrements"]), k
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax, w = g.truss_decomposition(work=True)
+            st = c.stats()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax
+            assert (st["peel_sum_min"], st["peel_decrements"]) == (w["sum_min"], w["decrements"])
