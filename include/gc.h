@@ -254,6 +254,11 @@ typedef enum gc_option {
                                  model's terms (gc_stats peel_sum_min,
                                  peel_decrements) at the cost of a few small kernels per
                                  round (default 0; measurement) */
+    GC_OPT_BUILD = 16,        /* gc_build_csr algorithm: 1 (default) buckets the raw pairs by
+                                 their low endpoint and the oriented edges by tail / head
+                                 (histogram, scan, scatter) and sorts each bucket with a
+                                 segmented sort; 0: global radix sorts of packed keys (the
+                                 round-1 build; testing) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

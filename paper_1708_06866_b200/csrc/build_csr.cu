@@ -15,6 +15,7 @@
 // Radix sorts are CUB's (library primitive); everything else is ours.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
@@ -241,6 +242,104 @@ __global__ void k_unpack_canon(const uint64_t* __restrict__ canon, int64_t m, in
     }
 }
 
+// ---- counting-sort build (GC_OPT_BUILD = 1): bucket by one endpoint with
+// a histogram, an exclusive scan and an atomic scatter, then sort each
+// bucket (CUB DeviceSegmentedSort: buckets are short -- a row of the graph
+// -- so each is sorted in registers / shared memory in one pass instead of
+// 3-6 global radix passes over every element).  Slots inside a bucket come
+// from atomic decrements, so the order before the segmented sort is
+// arbitrary; the sort makes the result deterministic (every rank of a
+// communicator builds the same CSR).
+
+// raw pairs per low endpoint (self loops dropped)
+__global__ void k_count_lo(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz,
+                           unsigned long long* __restrict__ cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
+        if (a != c) atomicAdd(cnt + min(a, c), 1ULL);
+    }
+}
+
+// key (lo << b) | hi into lo's bucket (slots taken from the bucket's end)
+__global__ void k_scatter_lo(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz, int b,
+                             const int64_t* __restrict__ ptr, unsigned long long* __restrict__ cnt,
+                             uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
+        if (a == c) continue;
+        const uint32_t lo = min(a, c), hi = max(a, c);
+        const int64_t slot = ptr[lo] + (int64_t)atomicAdd(cnt + lo, ~0ULL) - 1;   // atomic decrement
+        keys[slot] = ((uint64_t)lo << b) | hi;
+    }
+}
+
+// out-degree of every tail (lower rank) of the canonical edges
+__global__ void k_orient_count(const uint64_t* __restrict__ canon, int64_t m, int b,
+                               const int32_t* __restrict__ rank_of, unsigned long long* __restrict__ cnt) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = canon[e];
+        const uint32_t ra = (uint32_t)__ldg(rank_of + (k >> b)), rb = (uint32_t)__ldg(rank_of + (k & mask));
+        atomicAdd(cnt + min(ra, rb), 1ULL);
+    }
+}
+
+// (head << 32) | canonical id into the tail's row; the tail goes to dag_src
+__global__ void k_orient_scatter(const uint64_t* __restrict__ canon, int64_t m, int b,
+                                 const int32_t* __restrict__ rank_of, const int64_t* __restrict__ ptr,
+                                 unsigned long long* __restrict__ cnt, uint64_t* __restrict__ rows,
+                                 int32_t* __restrict__ dag_src) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = canon[e];
+        const uint32_t ra = (uint32_t)__ldg(rank_of + (k >> b)), rb = (uint32_t)__ldg(rank_of + (k & mask));
+        const uint32_t t = min(ra, rb), h = max(ra, rb);
+        const int64_t slot = ptr[t] + (int64_t)atomicAdd(cnt + t, ~0ULL) - 1;
+        rows[slot] = ((uint64_t)h << 32) | (uint32_t)e;
+        dag_src[slot] = (int32_t)t;
+    }
+}
+
+__global__ void k_split_rows(const uint64_t* __restrict__ rows, int64_t m, int32_t* __restrict__ col,
+                             int32_t* __restrict__ eid) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = rows[p];
+        col[p] = (int32_t)(x >> 32);
+        eid[p] = (int32_t)(uint32_t)x;
+    }
+}
+
+// in-degree of every head; lanes with the same head add once (a hub is the
+// head of many short rows that share a warp)
+__global__ void k_count_head(const int32_t* __restrict__ dag_col, int64_t m, unsigned long long* __restrict__ cnt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t h = dag_col[p];
+        const unsigned grp = __match_any_sync(__activemask(), h);
+        if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(cnt + h, (unsigned long long)__popc(grp));
+    }
+}
+
+// DAG position p into its head's in-list segment
+__global__ void k_in_scatter(const int32_t* __restrict__ dag_col, int64_t m, const int64_t* __restrict__ ptr,
+                             unsigned long long* __restrict__ cnt, uint32_t* __restrict__ pos) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t h = dag_col[p];
+        const int64_t slot = ptr[h] + (int64_t)atomicAdd(cnt + h, ~0ULL) - 1;
+        pos[slot] = (uint32_t)p;
+    }
+}
+
+// in-list entry i (DAG position p, sorted per head): tail and head
+__global__ void k_in_fill(const int32_t* __restrict__ in_pos, int64_t m, const int32_t* __restrict__ dag_src,
+                          const int32_t* __restrict__ dag_col, int32_t* __restrict__ in_src,
+                          int32_t* __restrict__ in_dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = in_pos[i];
+        in_src[i] = dag_src[p];
+        in_dst[i] = dag_col[p];
+    }
+}
+
 }  // namespace
 
 // Sort keys (and optional int32 payload) on bits [0, nbits); results in
@@ -298,11 +397,38 @@ static int radix_sort(gc_ctx* c, const uint64_t* kin, uint64_t* kout, const int3
     return GC_OK;
 }
 
+// ptr = exclusive scan of the n + 1 counts (cnt[n] = 0)
+static int scan_counts(gc_ctx* c, const unsigned long long* cnt, int64_t n, int64_t* ptr) {
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, n + 1, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cnt, ptr, n + 1, c->stream));
+    c->stats.lib_launches += 2;
+    return GC_OK;
+}
+
+// sort every segment [ptr[x], ptr[x+1]) of keys_in into keys_out
+template <class K>
+static int seg_sort(gc_ctx* c, const K* keys_in, K* keys_out, int64_t N, int64_t n, const int64_t* ptr) {
+    if (N <= 0) return GC_OK;
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys_in, keys_out, (int)N, (int)n, ptr, ptr + 1,
+                                                  c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->cub_tmp.p, tmp, keys_in, keys_out, (int)N, (int)n, ptr, ptr + 1,
+                                                  c->stream));
+    c->stats.lib_launches += 4;   // partition + small / medium + large segment kernels (estimate)
+    return GC_OK;
+}
+
 int build_csr(gc_ctx* c) {
     const int64_t nnz = c->nnz;
     c->n = 0;
     c->m = 0;
     c->bits = 1;
+    c->build_v2_done = false;
     GC_TRY(ensure(c, c->scal, 1024));
     int* d_scal = c->scal.as<int>();
     GC_TRY(host_scratch(c, 4096));
@@ -333,7 +459,40 @@ int build_csr(gc_ctx* c) {
         GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
         const uint64_t sent = (2 * b >= 64) ? ~0ULL : ((1ULL << (2 * b)) - 1);
         bool joined_done = false;
-        if (GC_SPLIT_SORT1 && b <= 31) {
+        if (c->build_mode == 1 && b <= 31 && n <= ((int64_t)1 << 31) - 2) {
+            // bucket the raw pairs by their low endpoint, sort each bucket, unique
+            GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+            GC_TRY(ensure(c, c->tmp_b, (size_t)(n + 1) * 8));
+            unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
+            int64_t* ptr = c->tmp_b.as<int64_t>();
+            GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
+            GC_LAUNCH(c, k_count_lo, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
+                      cnt);
+            GC_TRY(scan_counts(c, cnt, n, ptr));
+            GC_TRY(read_small(c, h, ptr + n, 8));
+            GC_TRY(sync(c));
+            const int64_t nv = h[0];                        // pairs that are no self loop
+            if (nv > 0) {
+                GC_LAUNCH(c, k_scatter_lo, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(),
+                          nnz, b, ptr, cnt, c->keys_a.as<uint64_t>());
+                GC_TRY(seg_sort<uint64_t>(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nv, n, ptr));
+                GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
+                int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
+                size_t tmp2 = 0;
+                GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp2, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
+                                                     d_nsel, nv, c->stream));
+                GC_TRY(ensure(c, c->cub_tmp, tmp2));
+                tmp2 = c->cub_tmp.cap;
+                GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp2, c->keys_b.as<uint64_t>(),
+                                                     c->canon.as<uint64_t>(), d_nsel, nv, c->stream));
+                c->stats.lib_launches += 2;
+                GC_TRY(read_small(c, h, d_nsel, 8));
+                GC_TRY(sync(c));
+                m = h[0];
+            }
+            joined_done = true;
+            c->build_v2_done = true;
+        } else if (GC_SPLIT_SORT1 && b <= 31) {
             // (lo, hi) order by two stable 32-bit pair sorts, hi then lo: the same
             // bytes per pass as one 64-bit key sort, with 32-bit digits passes
             uint32_t* lo_a = reinterpret_cast<uint32_t*>(c->keys_a.p);
@@ -370,7 +529,9 @@ int build_csr(gc_ctx* c) {
         }
         GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
         int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
-        if (!joined_done) {
+        if (c->build_v2_done) {
+            // m known, no self-loop sentinel in the list
+        } else if (!joined_done) {
             size_t tmp = 0;
             GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
                                                  d_nsel, nnz, c->stream));
@@ -380,6 +541,7 @@ int build_csr(gc_ctx* c) {
                                                  c->canon.as<uint64_t>(), d_nsel, nnz, c->stream));
             c->stats.lib_launches += 2;
         }
+        if (!c->build_v2_done) {
         GC_TRY(read_small(c, h, d_nsel, 8));
         GC_TRY(sync(c));
         int64_t nsel = h[0];
@@ -387,6 +549,7 @@ int build_csr(gc_ctx* c) {
             GC_TRY(read_small(c, h + 1, c->canon.as<uint64_t>() + nsel - 1, 8));
             GC_TRY(sync(c));
             m = nsel - ((uint64_t)h[1] == sent ? 1 : 0);
+        }
         }
     }
     if (m >= ((int64_t)1 << 31) - 1) return fail(c, GC_ERR_RANGE, "gc_build_csr: m >= 2^31 (edge ids are int32)");
@@ -440,13 +603,45 @@ int build_csr(gc_ctx* c) {
         c->stats.lib_launches += 2 + (dbits + 7) / 8;
         GC_LAUNCH(c, k_rank_scatter, grid_for(n), kThreads, 0, ids_out, n, c->rank_of.as<int32_t>());
     }
-    if (m > 0) {
+    if (c->build_mode == 1) {
+        // DAG rows: out-degree histogram, scan, scatter (head, id) into the
+        // tail's row, sort each row by head.  In-lists: in-degree histogram,
+        // scan, scatter the DAG position into the head's segment, sort each
+        // segment (DAG positions ascend with the tail).
+        GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+        unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
+        int64_t* dptr = c->dag_ptr.as<int64_t>();
+        int64_t* iptr = c->in_ptr.as<int64_t>();
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
+        if (m > 0)
+            GC_LAUNCH(c, k_orient_count, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b,
+                      c->rank_of.as<int32_t>(), cnt);
+        GC_TRY(scan_counts(c, cnt, n, dptr));
+        if (m > 0) {
+            GC_LAUNCH(c, k_orient_scatter, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b,
+                      c->rank_of.as<int32_t>(), dptr, cnt, c->keys_a.as<uint64_t>(), c->dag_src.as<int32_t>());
+            GC_TRY(seg_sort<uint64_t>(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), m, n, dptr));
+            GC_LAUNCH(c, k_split_rows, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, c->dag_col.as<int32_t>(),
+                      c->dag_eid.as<int32_t>());
+        }
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
+        if (m > 0) GC_LAUNCH(c, k_count_head, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), m, cnt);
+        GC_TRY(scan_counts(c, cnt, n, iptr));
+        if (m > 0) {
+            uint32_t* pos = reinterpret_cast<uint32_t*>(c->keys_a.p);
+            GC_LAUNCH(c, k_in_scatter, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), m, iptr, cnt, pos);
+            GC_TRY(seg_sort<uint32_t>(c, pos, reinterpret_cast<uint32_t*>(c->in_pos.p), m, n, iptr));
+            GC_LAUNCH(c, k_in_fill, grid_for(m), kThreads, 0, c->in_pos.as<int32_t>(), m, c->dag_src.as<int32_t>(),
+                      c->dag_col.as<int32_t>(), c->in_src.as<int32_t>(), c->in_dst.as<int32_t>());
+        }
+    }
+    if (m > 0 && c->build_mode != 1) {
         GC_LAUNCH(c, k_orient, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->rank_of.as<int32_t>(),
                   c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
         GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
                           c->dag_eid.as<int32_t>(), m, 2 * b));
     }
-    {
+    if (c->build_mode != 1) {
         // split the sorted keys into (dag_col, dag_src) and the row bounds in one pass;
         // keys_a is free after the sort: first / last there, row lengths in vals_a
         int32_t* first = reinterpret_cast<int32_t*>(c->keys_a.p);
@@ -459,7 +654,9 @@ int build_csr(gc_ctx* c) {
         GC_TRY(ptr_from_bounds(c, first, last, n, c->tmp_a.as<int64_t>(), c->dag_ptr.as<int64_t>()));
     }
     // in-lists: sort (head, tail) with the DAG position as payload
-    if (m > 0) {
+    if (c->build_mode == 1) {
+        // built above
+    } else if (m > 0) {
         // DAG order is sorted by (tail, head): a stable sort on the head alone
         // (b-bit keys, 32-bit) groups in-edges by head with tails ascending.
         uint64_t* pv = c->keys_a.as<uint64_t>();          // free after the orientation sort

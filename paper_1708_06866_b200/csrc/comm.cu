@@ -6,7 +6,9 @@
 // context stream:
 //   triangle count  ncclAllReduce(uint64, sum, 1)
 //   edge support    ncclAllReduce(uint32, sum, m)
-//   k-truss peel    ncclAllGather of the removed-edge bitmap (per round)
+//   k-truss peel    ncclAllGather of the removed-edge bitmap (per round; at a
+//                   level start also the zero-support bitmap and an
+//                   ncclAllReduce(min) of the smallest support left out)
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -116,6 +118,12 @@ int allreduce_u64(gc_ctx* c, uint64_t* dev, size_t count) {
 int allreduce_u32(gc_ctx* c, uint32_t* dev, size_t count) {
     ncclResult_t r = api().AllReduce(dev, dev, count, ncclUint32, ncclSum, static_cast<ncclComm_t>(c->nccl), c->stream);
     if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllReduce(u32)");
+    return GC_OK;
+}
+
+int allreduce_min_u32(gc_ctx* c, uint32_t* dev, size_t count) {
+    ncclResult_t r = api().AllReduce(dev, dev, count, ncclUint32, ncclMin, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllReduce(u32, min)");
     return GC_OK;
 }
 

@@ -246,7 +246,7 @@ int gc_destroy(gc_ctx* c) {
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->front_a,
-                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist,
+                        &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->zbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist,
                         &c->vdeg, &c->zlist};
     for (auto* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
@@ -285,11 +285,8 @@ int gc_comm_init(gc_ctx* c, const void* id, int nranks, int rank) {
     if (c->state != 0) return fail(c, GC_ERR_STATE, "gc_comm_init must precede gc_load_edges");
     if (c->nccl || c->loop_parts) return fail(c, GC_ERR_STATE, "communicator already initialised");
     cudaSetDevice(c->device);
-    if (nranks == 1) {
-        c->nranks = 1;
-        c->rank = 0;
-        return GC_OK;
-    }
+    // nranks == 1 forms a real one-rank communicator: every collective of the
+    // multi-GPU path (allreduce, in-place allgather) then runs through NCCL
     return nccl_init(c, id, nranks, rank);
 }
 
@@ -559,6 +556,10 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
             return GC_OK;
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;
+            return GC_OK;
+        case GC_OPT_BUILD:
+            if (value < 0 || value > 1) return fail(c, GC_ERR_INVALID, "build mode must be 0 or 1");
+            c->build_mode = (int)value;
             return GC_OK;
         case GC_OPT_WORK_STATS:
             c->work_stats = value ? 1 : 0;

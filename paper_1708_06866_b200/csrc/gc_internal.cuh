@@ -69,6 +69,8 @@ struct gc_ctx {
 
     // options
     int force_class = -1;
+    int build_mode = 0;              // GC_OPT_BUILD: 1 counting-sort build (bucket + segmented sort), 0 global radix sorts
+    bool build_v2_done = false;      // the last build's canonicalisation took the counting-sort path
     int64_t task_chunk = 32768;
     int timing = 1;
     int block_bitmap = 1;
@@ -159,6 +161,7 @@ struct gc_ctx {
     gcx::Buf tau;       // int32[m]
     gcx::Buf xbits;     // uint32 removed-edge bitmap X of the round (partitioned peel, allgathered)
     gcx::Buf nbits;     // uint32 next-round bitmap (each owner sets bits in its slice)
+    gcx::Buf zbits;     // uint32 zero-support edges of a level start (removed without enumeration)
     gcx::Buf sup_parts; // uint32[P*m] per-virtual-rank supports (loopback partitions only)
     int peel_part = 0;  // 1: partitioned (bitmap) peeler even on one rank (GC_OPT_PEEL_PART)
     int work_stats = 0; // GC_OPT_WORK_STATS: count the k-truss byte model's terms while peeling
@@ -226,6 +229,7 @@ int nccl_init(gc_ctx* c, const void* id, int nranks, int rank);
 int nccl_destroy(gc_ctx* c);
 int allreduce_u64(gc_ctx* c, uint64_t* dev, size_t count);
 int allreduce_u32(gc_ctx* c, uint32_t* dev, size_t count);
+int allreduce_min_u32(gc_ctx* c, uint32_t* dev, size_t count);
 int allgather_u32(gc_ctx* c, const uint32_t* send, uint32_t* recv, size_t count_per_rank);
 
 inline int ceil_log2_u64(uint64_t x) {  // bits needed to represent values < x (x >= 1)

@@ -621,16 +621,50 @@ __global__ void __launch_bounds__(256, GC_GRP_MINB) k_peel_grouped(PeelArgs A, P
 // (ncclAllGather of each owner's slice), every rank enumerates the destroyed
 // triangles of the whole X and decrements only the survivors it owns.
 
-// own slice of X at a level start: bit e = alive[e] && S[e] < thr, e in [lo, hi)
+// own slices at a level start, e in [lo, hi): X bit = alive && 0 < S < thr
+// (the round's frontier), Z bit = alive && S == 0 < thr (in no live triangle:
+// removed on every rank without enumeration), and min S over the owned
+// alive edges left out (the empty-level skip)
 __global__ void k_front_bits(const uint32_t* __restrict__ S, const uint8_t* __restrict__ alive, int64_t lo,
-                             int64_t hi, uint32_t thr, uint32_t* __restrict__ bits) {
+                             int64_t hi, uint32_t thr, uint32_t* __restrict__ xbits, uint32_t* __restrict__ zbits,
+                             uint32_t* __restrict__ min_rest) {
     // lo is a multiple of 32: thread e's ballot is word e / 32
+    uint32_t rest = 0xFFFFFFFFu;
     for (int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < lo + (((hi - lo) + 31) & ~(int64_t)31);
          e += (int64_t)gridDim.x * blockDim.x) {
-        const bool in = e < hi && alive[e] && S[e] < thr;
-        const unsigned w = __ballot_sync(0xffffffffu, in);
-        if ((threadIdx.x & 31) == 0) bits[e >> 5] = w;
+        const bool al = e < hi && alive[e];
+        const uint32_t se = al ? S[e] : 0xFFFFFFFFu;
+        const bool zero = al && se == 0 && thr > 0;
+        const bool in = al && se > 0 && se < thr;
+        if (al && !zero && !in) rest = min(rest, se);
+        const unsigned wx = __ballot_sync(0xffffffffu, in);
+        const unsigned wz = __ballot_sync(0xffffffffu, zero);
+        if ((threadIdx.x & 31) == 0) {
+            xbits[e >> 5] = wx;
+            zbits[e >> 5] = wz;
+        }
     }
+    rest = __reduce_min_sync(0xffffffffu, rest);
+    if ((threadIdx.x & 31) == 0 && rest != 0xFFFFFFFFu) atomicMin(min_rest, rest);
+}
+
+// the gathered zero-support edges leave (every rank): alive = 0, tau = level
+__global__ void k_zero_finish(const uint32_t* __restrict__ zbits, int64_t nwords, uint8_t* __restrict__ alive,
+                              int32_t* __restrict__ tau, int32_t level, unsigned long long* __restrict__ acc) {
+    unsigned c = 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t x = zbits[w];
+        c += __popc(x);
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            const int64_t e = w * 32 + b;
+            alive[e] = 0;
+            if (tau) tau[e] = level;
+        }
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(acc, (unsigned long long)c);
 }
 
 // list of the set bits of bits[0, nwords) (order unspecified)
@@ -1063,7 +1097,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
 
 // ---- partitioned peel (multi-GPU v1; loopback virtual ranks on one GPU)
 static int peel_parts(const gc_ctx* c) {
-    if (c->nccl && c->nranks > 1) return c->nranks;
+    if (c->nccl) return c->nranks;            // a real communicator (one rank included)
     if (c->loop_parts > 1) return c->loop_parts;
     return c->peel_part ? 1 : 0;   // 0: single-GPU frontier-list peeler
 }
@@ -1075,49 +1109,113 @@ static uint32_t* part_support(gc_ctx* c, int r) {
     return c->sup.as<uint32_t>();
 }
 
-static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* removed) {
+// One level of the partitioned peel.  At the level start each owner scans
+// its range into the frontier bitmap X and the zero-support bitmap Z; both
+// are allgathered, Z's edges leave on every rank without enumeration (they
+// lie in no live triangle), and min S over the edges left out is combined
+// (ncclAllReduce min) for the empty-level skip.  Rounds then run in
+// device-side batches like the single-rank peeler: each round lists the
+// gathered X, enumerates its destroyed triangles (owner-only decrements;
+// crossings set bits of the next X), removes X and allgathers the next X,
+// with no host round trip inside a batch; the host reads the next frontier
+// size after each batch.  Every rank sees the same gathered bitmaps, so
+// every rank takes the same batch decisions and issues the same collectives.
+static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* removed, uint32_t* next_thr) {
     const int64_t m = c->m;
     const int P = peel_parts(c);
     const int64_t W = part_words(c, P);
-    const bool nccl = c->nccl && c->nranks > 1;
+    const bool nccl = c->nccl != nullptr;
     const int r_begin = nccl ? c->rank : 0, r_end = nccl ? c->rank + 1 : P;
-    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);      // two frontier counts
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 256);   // removed, rounds
+    unsigned long long* zrem = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 240);
+    uint32_t* min_rest = reinterpret_cast<uint32_t*>(c->scal.as<char>() + 320);
     int32_t* h = static_cast<int32_t*>(c->hpin);
     uint32_t* xb = c->xbits.as<uint32_t>();
     uint32_t* nb = c->nbits.as<uint32_t>();
-    int32_t* front = c->front_a.as<int32_t>();
+    uint32_t* zb = c->zbits.as<uint32_t>();
+    int32_t* lists[2] = {c->front_a.as<int32_t>(), c->front_b.as<int32_t>()};
+    int* counts[2] = {cnt, cnt + 1};
+    int32_t* tau = level >= 0 ? c->tau.as<int32_t>() : nullptr;
     *removed = 0;
     auto lo_of = [&](int r) { return std::min<int64_t>(m, (int64_t)r * W * 32); };
     auto hi_of = [&](int r) { return std::min<int64_t>(m, (int64_t)(r + 1) * W * 32); };
-    // X at the level start: each owner scans its range
     GC_TRY(maybe_compact(c));
+    GC_TRY(record(c, 10));
     GC_CUDA(c, cudaMemsetAsync(xb, 0, (size_t)P * W * 4, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(zb, 0, (size_t)P * W * 4, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(min_rest, 0xFF, 4, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(zrem, 0, 8, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(acc, 0, 16, c->stream));
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c->stream));
     for (int r = r_begin; r < r_end; ++r)
         if (hi_of(r) > lo_of(r))
             GC_LAUNCH(c, k_front_bits, grid_for(hi_of(r) - lo_of(r)), kThreads, 0, part_support(c, r),
-                      c->alive.as<uint8_t>(), lo_of(r), hi_of(r), thr, xb);
-    for (;;) {
-        if (nccl) GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
-        GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
-        GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, front, cnt);
-        GC_TRY(read_small(c, h, cnt, sizeof(int)));
-        GC_TRY(sync(c));
-        const int nf = h[0];
-        if (nf == 0) break;
-        GC_TRY(ensure_rows(c));
-        GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
-        for (int r = r_begin; r < r_end; ++r) {
-            PolicyPart pol{xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb};
-            GC_TRY(peel_round(c, front, nf, pol));
-        }
-        GC_LAUNCH(c, k_finish_round, grid_for(nf), kThreads, 0, front, nf, c->alive.as<uint8_t>(),
-                  level >= 0 ? c->tau.as<int32_t>() : nullptr, level);
-        *removed += nf;
-        c->m_alive_h -= nf;
-        c->stats.peel_rounds++;
-        std::swap(xb, nb);
-        GC_TRY(maybe_compact(c));
+                      c->alive.as<uint8_t>(), lo_of(r), hi_of(r), thr, xb, zb, min_rest);
+    if (nccl) {
+        GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
+        GC_TRY(allgather_u32(c, zb + (size_t)c->rank * W, zb, (size_t)W));
+        GC_TRY(allreduce_min_u32(c, min_rest, 1));
     }
+    GC_LAUNCH(c, k_zero_finish, grid_for(P * W), kThreads, 0, zb, P * W, c->alive.as<uint8_t>(), tau, level, zrem);
+    GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, lists[0], counts[0]);
+    GC_TRY(record(c, 11));
+    GC_TRY(read_small(c, h, counts[0], sizeof(int)));
+    GC_TRY(read_small(c, h + 2, zrem, 8));
+    GC_TRY(read_small(c, h + 4, min_rest, 4));
+    GC_TRY(sync(c));
+    c->stats.scan_ms += elapsed(c, 10, 11);
+    {
+        const int64_t z = *reinterpret_cast<int64_t*>(h + 2);
+        *removed += z;
+        c->m_alive_h -= z;
+    }
+    int nf = h[0];
+    if (next_thr) {
+        const uint32_t mr = static_cast<uint32_t>(h[4]);
+        *next_thr = nf > 0 ? 0u : (mr == 0xFFFFFFFFu ? 0u : mr + 1);
+    }
+    if (nf > 0) GC_TRY(ensure_rows(c));
+    const int64_t alive0 = c->m_alive_h;
+    int cur = 0, batch = c->trace > 1 ? 1 : 2, last_nf = nf;
+    unsigned long long done[2] = {0, 0};
+    while (nf > 0) {
+        GC_TRY(record(c, 8));
+        for (int b = 0; b < batch; ++b) {
+            const int nxt = cur ^ 1;
+            GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
+            for (int r = r_begin; r < r_end; ++r) {
+                PolicyPart pol{xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb};
+                PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                           c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                           c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
+                GC_TRY(launch_peel(c, 148 * 8, A, pol, b == 0 ? (int64_t)nf : 0));
+            }
+            GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
+                      tau, level, acc);
+            std::swap(xb, nb);
+            if (nccl) GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
+            GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
+            GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, lists[nxt], counts[nxt]);
+            cur = nxt;
+        }
+        GC_TRY(record(c, 9));
+        GC_TRY(read_small(c, h, counts[cur], sizeof(int)));
+        GC_TRY(read_small(c, h + 2, acc, 16));
+        GC_TRY(sync(c));
+        c->stats.peel_kernel_ms += elapsed(c, 8, 9);
+        memcpy(done, h + 2, 16);
+        if (c->trace)
+            fprintf(stderr, "peel-trace part level %d batch %d nf %d rounds %llu removed %llu ms %.4f\n", level, batch,
+                    nf, done[1], done[0], elapsed(c, 8, 9));
+        c->m_alive_h = alive0 - (int64_t)done[0];
+        nf = h[0];
+        if (nf > 0) GC_TRY(maybe_compact(c));
+        if (c->trace < 2) batch = (nf >= kBatchMaxFront || nf > last_nf) ? 1 : std::min(batch * 2, 16);
+        last_nf = nf;
+    }
+    *removed += (int64_t)done[0];
+    c->stats.peel_rounds += (int64_t)done[1];
     return GC_OK;
 }
 
@@ -1153,6 +1251,7 @@ static int peel_setup(gc_ctx* c) {
         const int64_t W = part_words(c, P);
         GC_TRY(ensure(c, c->xbits, (size_t)P * W * 4));
         GC_TRY(ensure(c, c->nbits, (size_t)P * W * 4));
+        GC_TRY(ensure(c, c->zbits, (size_t)P * W * 4));
         if (c->loop_parts > 1 && m > 0) {
             // every virtual rank starts from the combined exact support
             GC_TRY(ensure(c, c->sup_parts, (size_t)P * m * 4));
@@ -1167,7 +1266,7 @@ static int peel_setup(gc_ctx* c) {
 static int peel_any(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, int64_t* removed,
                     uint32_t* next_thr = nullptr) {
     if (next_thr) *next_thr = 0;
-    if (peel_parts(c) > 0) return peel_level_part(c, thr, level, removed);
+    if (peel_parts(c) > 0) return peel_level_part(c, thr, level, removed, next_thr);
     return peel_level(c, thr, level, round, removed, next_thr);
 }
 

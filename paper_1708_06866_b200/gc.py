@@ -44,6 +44,7 @@ GC_OPT_GROUP_PEEL = 12
 GC_OPT_GROUP_HEAVY = 14
 GC_OPT_OVERLAP = 13
 GC_OPT_WORK_STATS = 15
+GC_OPT_BUILD = 16
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [

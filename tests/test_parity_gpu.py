@@ -785,3 +785,61 @@ def test_work_stats_match_oracle_replay(gcmod):
             st = c.stats()
             assert np.array_equal(tau, want_tau) and kmax == want_kmax
             assert (st["peel_sum_min"], st["peel_decrements"]) == (w["sum_min"], w["decrements"])
+
+
+# ------------------------------------------------- NCCL on the hardware (§8(e)) --
+def test_nccl_one_rank_communicator(gcmod):
+    """A real one-rank NCCL communicator (gc_comm_init, nranks = 1; NCCL resolved
+    by dlopen): the triangle count and support passes end in ncclAllReduce, the
+    peeler is the partitioned one (removed-edge bitmap per round through the
+    in-place ncclAllGather, zero-support bitmap and ncclAllReduce(min) at each
+    level start) — results equal the oracle's."""
+    cases = [gen.CONFIGS["C1"].generate(), gen.rmat(12, 16, seed=81)]
+    d = json.load(open(os.path.join(GOLDEN, "k4_ear.json")))
+    cases.append((np.array(d["raw_u"], np.int32), np.array(d["raw_v"], np.int32)))
+    for u, v in cases:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            c.comm_init(gcmod.nccl_unique_id(), 1, 0)
+            c.load_edges(u, v)
+            c.build_csr()
+            assert c.triangle_count() == g.triangle_count()
+            assert np.array_equal(c.edge_support(), g.support())
+            for k in (3, 4, 6):
+                want, _ = g.ktruss(k)
+                mask, m_alive = c.ktruss(k)
+                assert np.array_equal(mask, want) and m_alive == int(want.sum()), k
+            T, sup, mask, _ = c.ktruss_analysis(5)
+            assert T == g.triangle_count() and np.array_equal(mask, g.ktruss(5)[0])
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax = g.truss_decomposition()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax
+            assert c.stats()["peel_rounds"] > 0 or want_kmax <= 3
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_build_modes(gcmod, mode):
+    """Both gc_build_csr algorithms (GC_OPT_BUILD: 1 bucket + segmented sort,
+    0 global radix sorts) give the oracle's canonical list, supports and
+    k-trusses, on graphs with duplicates, reversed pairs, self loops, an
+    isolated top id, a hub, and the degenerate inputs."""
+    rng = np.random.default_rng(90 + mode)
+    hub_u = np.zeros(3000, np.int32)
+    hub_v = rng.integers(1, 5000, 3000).astype(np.int32)
+    cases = [gen.CONFIGS["C1"].generate(), gen.rmat(13, 16, seed=91), (hub_u, hub_v),
+             (np.array([5, 5, 2, 9, 2], np.int32), np.array([5, 2, 5, 1 << 20, 2], np.int32)),
+             (np.array([3, 3], np.int32), np.array([3, 3], np.int32)),
+             (np.zeros(0, np.int32), np.zeros(0, np.int32))]
+    for u, v in cases:
+        g = oracle.OracleGraph(u, v)
+        with gcmod.Context(0) as c:
+            c.set_option(gcmod.GC_OPT_BUILD, mode)
+            c.load_edges(u, v)
+            c.build_csr()
+            assert (c.num_vertices(), c.num_edges()) == (g.n, g.m)
+            cu, cv = c.get_edges()
+            assert np.array_equal(cu, g.cu) and np.array_equal(cv, g.cv)
+            assert c.triangle_count() == g.triangle_count()
+            assert np.array_equal(c.edge_support(), g.support())
+            want, _ = g.ktruss(4)
+            assert np.array_equal(c.ktruss(4)[0], want)
