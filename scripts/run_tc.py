@@ -12,6 +12,7 @@ p.add_argument("--config", default="C3")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--what", default="tc,support")
 p.add_argument("--chunk", type=int, default=0)
+p.add_argument("--k", type=int, default=3, help="k of the analysis / ktruss calls")
 p.add_argument("--opt", action="append", default=[], help="OPTION_ID=VALUE (gc_set_option)")
 a = p.parse_args()
 u, v = gen.CONFIGS[a.config].generate()
@@ -29,9 +30,9 @@ for r in range(a.reps):
     if "support" in a.what:
         ctx.edge_support(torch.empty(ctx.num_edges(), dtype=torch.int32, device="cuda"))
     if "analysis" in a.what:
-        ctx.ktruss_analysis(3, torch.empty(ctx.num_edges(), dtype=torch.int32, device="cuda"),
+        ctx.ktruss_analysis(a.k, torch.empty(ctx.num_edges(), dtype=torch.int32, device="cuda"),
                             torch.empty(ctx.num_edges(), dtype=torch.uint8, device="cuda"))
     if "ktruss" in a.what:
-        ctx.ktruss(3, torch.empty(ctx.num_edges(), dtype=torch.uint8, device="cuda"))
+        ctx.ktruss(a.k, torch.empty(ctx.num_edges(), dtype=torch.uint8, device="cuda"))
     st = ctx.stats()
     print({k: st[k] for k in ["build_ms", "tc_kernel_ms", "support_kernel_ms", "ktruss_ms", "peel_ms", "tasks"]}, flush=True)

@@ -843,3 +843,4 @@ def test_build_modes(gcmod, mode):
             assert np.array_equal(c.edge_support(), g.support())
             want, _ = g.ktruss(4)
             assert np.array_equal(c.ktruss(4)[0], want)
+
