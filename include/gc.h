@@ -254,11 +254,10 @@ typedef enum gc_option {
                                  model's terms (gc_stats peel_sum_min,
                                  peel_decrements) at the cost of a few small kernels per
                                  round (default 0; measurement) */
-    GC_OPT_BUILD = 16,        /* gc_build_csr algorithm: 1 (default) buckets the raw pairs by
-                                 their low endpoint and the oriented edges by tail / head
-                                 (histogram, scan, scatter) and sorts each bucket with a
-                                 segmented sort; 0: global radix sorts of packed keys (the
-                                 round-1 build; testing) */
+    GC_OPT_BUILD_PART = 16,   /* gc_build_csr across owners: -1 (default)
+                                 partitioned when there are several owners (NCCL ranks or
+                                 loopback parts), 1 always (one owner included; testing),
+                                 0 never (every rank builds the whole CSR) */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 
@@ -293,6 +292,11 @@ typedef struct gc_stats {
                                  edges (a,b) with support > 0, of min(d(a), d(b)) (alive
                                  degrees at the round start); -1 when not counted */
     int64_t peel_decrements;  /* ... support decrements D applied to surviving edges; -1 */
+    double part_ms[16];       /* loopback partitions: intersection-kernel time of each virtual
+                                 rank in the last triangle-count / support pass (balance of
+                                 the 1D cost cut; ranks >= 16 not recorded) */
+    double part_build_ms[16]; /* loopback partitions: device time of each virtual rank's share
+                                 of the last partitioned gc_build_csr (its three sorts) */
 } gc_stats;
 int gc_get_stats(const gc_ctx* ctx, gc_stats* out);
 int gc_reset_stats(gc_ctx* ctx);

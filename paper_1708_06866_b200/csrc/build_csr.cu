@@ -15,7 +15,6 @@
 // Radix sorts are CUB's (library primitive); everything else is ours.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
@@ -242,40 +241,38 @@ __global__ void k_unpack_canon(const uint64_t* __restrict__ canon, int64_t m, in
     }
 }
 
-// ---- counting-sort build (GC_OPT_BUILD = 1): bucket by one endpoint with
-// a histogram, an exclusive scan and an atomic scatter, then sort each
-// bucket (CUB DeviceSegmentedSort: buckets are short -- a row of the graph
-// -- so each is sorted in registers / shared memory in one pass instead of
-// 3-6 global radix passes over every element).  Slots inside a bucket come
-// from atomic decrements, so the order before the segmented sort is
-// arbitrary; the sort makes the result deterministic (every rank of a
-// communicator builds the same CSR).
-
-// raw pairs per low endpoint (self loops dropped)
-__global__ void k_count_lo(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz,
-                           unsigned long long* __restrict__ cnt) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
-        if (a != c) atomicAdd(cnt + min(a, c), 1ULL);
-    }
-}
-
-// key (lo << b) | hi into lo's bucket (slots taken from the bucket's end)
-__global__ void k_scatter_lo(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz, int b,
-                             const int64_t* __restrict__ ptr, unsigned long long* __restrict__ cnt,
-                             uint64_t* __restrict__ keys) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
-        if (a == c) continue;
-        const uint32_t lo = min(a, c), hi = max(a, c);
-        const int64_t slot = ptr[lo] + (int64_t)atomicAdd(cnt + lo, ~0ULL) - 1;   // atomic decrement
-        keys[slot] = ((uint64_t)lo << b) | hi;
+// ---- partitioned build: per-owner selection kernels
+// raw pairs of owner range lo in [Llo, Lhi) as split (lo, hi) halves; order
+// of appends arbitrary (the pair sorts order them fully)
+__global__ void k_pack_range(const int32_t* __restrict__ u, const int32_t* __restrict__ v, int64_t nnz, uint32_t Llo,
+                             uint32_t Lhi, uint32_t* __restrict__ lo_out, uint32_t* __restrict__ hi_out,
+                             unsigned long long* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < nnz; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        uint32_t lo = 0, hi = 0;
+        bool in = false;
+        if (i < nnz) {
+            const uint32_t a = (uint32_t)__ldg(u + i), c = (uint32_t)__ldg(v + i);
+            lo = min(a, c);
+            hi = max(a, c);
+            in = a != c && lo >= Llo && lo < Lhi;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd(count, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (in) {
+            const unsigned long long o = base + __popc(bal & ((1u << lane) - 1));
+            lo_out[o] = lo;
+            hi_out[o] = hi;
+        }
     }
 }
 
 // out-degree of every tail (lower rank) of the canonical edges
-__global__ void k_orient_count(const uint64_t* __restrict__ canon, int64_t m, int b,
-                               const int32_t* __restrict__ rank_of, unsigned long long* __restrict__ cnt) {
+__global__ void k_tail_count(const uint64_t* __restrict__ canon, int64_t m, int b, const int32_t* __restrict__ rank_of,
+                             unsigned long long* __restrict__ cnt) {
     const uint64_t mask = (1ULL << b) - 1;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t k = canon[e];
@@ -284,34 +281,8 @@ __global__ void k_orient_count(const uint64_t* __restrict__ canon, int64_t m, in
     }
 }
 
-// (head << 32) | canonical id into the tail's row; the tail goes to dag_src
-__global__ void k_orient_scatter(const uint64_t* __restrict__ canon, int64_t m, int b,
-                                 const int32_t* __restrict__ rank_of, const int64_t* __restrict__ ptr,
-                                 unsigned long long* __restrict__ cnt, uint64_t* __restrict__ rows,
-                                 int32_t* __restrict__ dag_src) {
-    const uint64_t mask = (1ULL << b) - 1;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = canon[e];
-        const uint32_t ra = (uint32_t)__ldg(rank_of + (k >> b)), rb = (uint32_t)__ldg(rank_of + (k & mask));
-        const uint32_t t = min(ra, rb), h = max(ra, rb);
-        const int64_t slot = ptr[t] + (int64_t)atomicAdd(cnt + t, ~0ULL) - 1;
-        rows[slot] = ((uint64_t)h << 32) | (uint32_t)e;
-        dag_src[slot] = (int32_t)t;
-    }
-}
-
-__global__ void k_split_rows(const uint64_t* __restrict__ rows, int64_t m, int32_t* __restrict__ col,
-                             int32_t* __restrict__ eid) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t x = rows[p];
-        col[p] = (int32_t)(x >> 32);
-        eid[p] = (int32_t)(uint32_t)x;
-    }
-}
-
-// in-degree of every head; lanes with the same head add once (a hub is the
-// head of many short rows that share a warp)
-__global__ void k_count_head(const int32_t* __restrict__ dag_col, int64_t m, unsigned long long* __restrict__ cnt) {
+// in-degree of every head (lanes with the same head add once)
+__global__ void k_head_count(const int32_t* __restrict__ dag_col, int64_t m, unsigned long long* __restrict__ cnt) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t h = dag_col[p];
         const unsigned grp = __match_any_sync(__activemask(), h);
@@ -319,25 +290,73 @@ __global__ void k_count_head(const int32_t* __restrict__ dag_col, int64_t m, uns
     }
 }
 
-// DAG position p into its head's in-list segment
-__global__ void k_in_scatter(const int32_t* __restrict__ dag_col, int64_t m, const int64_t* __restrict__ ptr,
-                             unsigned long long* __restrict__ cnt, uint32_t* __restrict__ pos) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t h = dag_col[p];
-        const int64_t slot = ptr[h] + (int64_t)atomicAdd(cnt + h, ~0ULL) - 1;
-        pos[slot] = (uint32_t)p;
+// owner cut points: cut[r] = first row x with ptr[x] >= r * total / parts (r = 0..parts)
+__global__ void k_cuts(const int64_t* __restrict__ ptr, int64_t n, int parts, int64_t* __restrict__ cut) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > parts) return;
+    const int64_t total = ptr[n];
+    const int64_t want = (int64_t)((__int128)total * r / parts);
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ptr[mid] < want) lo = mid + 1; else hi = mid;
+    }
+    cut[r] = r == parts ? n : lo;
+}
+
+// canonical edges whose tail lies in [Tlo, Thi): oriented key + canonical id
+struct TailInRange {
+    const uint64_t* canon;
+    const int32_t* rank_of;
+    int b;
+    uint32_t Tlo, Thi;
+    __device__ bool operator()(int32_t e) const {
+        const uint64_t k = canon[e];
+        const uint32_t ra = (uint32_t)rank_of[k >> b], rb = (uint32_t)rank_of[k & ((1ULL << b) - 1)];
+        const uint32_t t = min(ra, rb);
+        return t >= Tlo && t < Thi;
+    }
+};
+
+__global__ void k_orient_sel(const uint64_t* __restrict__ canon, const int32_t* __restrict__ sel, int64_t cnt, int b,
+                             const int32_t* __restrict__ rank_of, uint64_t* __restrict__ keys) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = canon[sel[i]];
+        const uint32_t ra = (uint32_t)__ldg(rank_of + (k >> b)), rb = (uint32_t)__ldg(rank_of + (k & mask));
+        keys[i] = ((uint64_t)min(ra, rb) << b) | max(ra, rb);
     }
 }
 
-// in-list entry i (DAG position p, sorted per head): tail and head
-__global__ void k_in_fill(const int32_t* __restrict__ in_pos, int64_t m, const int32_t* __restrict__ dag_src,
-                          const int32_t* __restrict__ dag_col, int32_t* __restrict__ in_src,
-                          int32_t* __restrict__ in_dst) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t p = in_pos[i];
-        in_src[i] = dag_src[p];
-        in_dst[i] = dag_col[p];
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, int64_t cnt, int b, int32_t* __restrict__ col,
+                             int32_t* __restrict__ row) {
+    const uint64_t mask = (1ULL << b) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        row[i] = (int32_t)(k >> b);
+        col[i] = (int32_t)(k & mask);
     }
+}
+
+struct HeadInRange {
+    const int32_t* dag_col;
+    int32_t Hlo, Hhi;
+    __device__ bool operator()(int32_t p) const {
+        const int32_t h = dag_col[p];
+        return h >= Hlo && h < Hhi;
+    }
+};
+
+__global__ void k_gather_heads(const int32_t* __restrict__ sel, int64_t cnt, const int32_t* __restrict__ dag_col,
+                               uint32_t* __restrict__ heads) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        heads[i] = (uint32_t)dag_col[sel[i]];
+}
+
+__global__ void k_in_tail(const int32_t* __restrict__ pos, int64_t cnt, const int32_t* __restrict__ dag_src,
+                          int32_t* __restrict__ tail) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        tail[i] = dag_src[pos[i]];
 }
 
 }  // namespace
@@ -397,29 +416,258 @@ static int radix_sort(gc_ctx* c, const uint64_t* kin, uint64_t* kout, const int3
     return GC_OK;
 }
 
-// ptr = exclusive scan of the n + 1 counts (cnt[n] = 0)
-static int scan_counts(gc_ctx* c, const unsigned long long* cnt, int64_t n, int64_t* ptr) {
+// ------------------------------------------------------ partitioned build --
+// the three sorts of the build are cut between the owners
+// (NCCL ranks, or loopback virtual ranks on one GPU): owner r sorts only the
+// raw pairs whose low endpoint falls in its id range, the oriented edges whose
+// tail falls in its rank range, and the in-edges whose head falls in its
+// rank range (ranges cut at equal edge counts from the replicated row
+// pointers); the sorted parts are concatenated on every rank (NCCL: a
+// variable-size allgather per array).  The O(n) / O(m) counting passes
+// (degrees, row pointers, cut points) stay replicated.
+static int build_owners(const gc_ctx* c) {
+    if (c->loop_parts > 1) return c->loop_parts;
+    return c->nccl ? c->nranks : 1;
+}
+static bool part_build(const gc_ctx* c) {
+    if (c->build_part >= 0) return c->build_part == 1;
+    return build_owners(c) > 1;
+}
+
+// per-owner device time of the partitioned stages (loopback: stats.part_build_ms)
+struct OwnerTimer {
+    gc_ctx* c;
+    bool on;
+    int nt;
+    explicit OwnerTimer(gc_ctx* cc) : c(cc), on(cc->timing && cc->loop_parts > 1), nt(std::min(cc->loop_parts, 16)) {}
+    int begin(int r) {
+        if (!on || r >= nt) return GC_OK;
+        if (!c->pev[r]) GC_CUDA(c, cudaEventCreate(&c->pev[r]));
+        if (!c->pev[16]) GC_CUDA(c, cudaEventCreate(&c->pev[16]));
+        GC_CUDA(c, cudaEventRecord(c->pev[r], c->stream));
+        return GC_OK;
+    }
+    int end(int r) {
+        if (!on || r >= nt) return GC_OK;
+        GC_CUDA(c, cudaEventRecord(c->pev[16], c->stream));
+        GC_CUDA(c, cudaEventSynchronize(c->pev[16]));
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->pev[r], c->pev[16]) != cudaSuccess) cudaGetLastError();
+        c->stats.part_build_ms[r] += ms;
+        return GC_OK;
+    }
+};
+
+template <class Pred>
+static int select_iota(gc_ctx* c, int64_t N, Pred pred, int32_t* out, int64_t* d_count) {
+    thrust::counting_iterator<int32_t> iota(0);
     size_t tmp = 0;
-    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, ptr, n + 1, c->stream));
+    GC_CUDA(c, cub::DeviceSelect::If(nullptr, tmp, iota, out, d_count, N, pred, c->stream));
     GC_TRY(ensure(c, c->cub_tmp, tmp));
     tmp = c->cub_tmp.cap;
-    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cnt, ptr, n + 1, c->stream));
+    GC_CUDA(c, cub::DeviceSelect::If(c->cub_tmp.p, tmp, iota, out, d_count, N, pred, c->stream));
     c->stats.lib_launches += 2;
     return GC_OK;
 }
 
-// sort every segment [ptr[x], ptr[x+1]) of keys_in into keys_out
-template <class K>
-static int seg_sort(gc_ctx* c, const K* keys_in, K* keys_out, int64_t N, int64_t n, const int64_t* ptr) {
-    if (N <= 0) return GC_OK;
+// cut points of `parts` owners over row pointers ptr[0..n] (host copy in cut_h)
+static int owner_cuts(gc_ctx* c, const int64_t* ptr, int64_t n, int parts, int64_t* cut_h, int64_t* base_h) {
+    GC_TRY(ensure(c, c->tmp_b, (size_t)(parts + 1) * 8));
+    int64_t* cut = c->tmp_b.as<int64_t>();
+    GC_LAUNCH(c, k_cuts, 1, 128, 0, ptr, n, parts, cut);
+    int64_t* h = static_cast<int64_t*>(c->hpin);
+    GC_TRY(read_small(c, h, cut, (size_t)(parts + 1) * 8));
+    GC_TRY(sync(c));
+    for (int r = 0; r <= parts; ++r) cut_h[r] = h[r];
+    for (int r = 0; r <= parts; ++r) GC_TRY(read_small(c, h + 128 + r, ptr + cut_h[r], 8));
+    GC_TRY(sync(c));
+    for (int r = 0; r <= parts; ++r) base_h[r] = h[128 + r];
+    return GC_OK;
+}
+
+// a2 across owners: canon = concatenation of the owners' sorted unique parts
+static int part_canonical(gc_ctx* c, int64_t nnz, int64_t n, int b, int64_t* m_out) {
+    const int P = build_owners(c);
+    const bool nccl = c->nccl != nullptr;
+    const int r0 = nccl ? c->rank : 0, r1 = nccl ? c->rank + 1 : P;
+    int64_t* h = static_cast<int64_t*>(c->hpin);
+    uint32_t* lo_a = reinterpret_cast<uint32_t*>(c->keys_a.p);
+    uint32_t* hi_a = lo_a + nnz;
+    uint32_t* lo_b = reinterpret_cast<uint32_t*>(c->keys_b.p);
+    uint32_t* hi_b = lo_b + nnz;
+    GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
+    GC_TRY(ensure(c, c->tmp_a, (size_t)nnz * 8 + 8));
+    uint64_t* part = c->tmp_a.as<uint64_t>();               // this owner's unique keys
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 960);
+    int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 968);
+    OwnerTimer tm(c);
+    int64_t off = 0, mine = 0;
+    for (int r = r0; r < r1; ++r) {
+        GC_TRY(tm.begin(r));
+        const uint32_t Llo = (uint32_t)(n * r / P), Lhi = (uint32_t)(n * (r + 1) / P);
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, 8, c->stream));
+        GC_LAUNCH(c, k_pack_range, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
+                  Llo, Lhi, lo_a, hi_a, cnt);
+        GC_TRY(read_small(c, h, cnt, 8));
+        GC_TRY(sync(c));
+        const int64_t k = h[0];
+        int64_t mr = 0;
+        if (k > 0) {
+            size_t tmp = 0;
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, hi_a, hi_b, lo_a, lo_b, k, 0, b, c->stream));
+            GC_TRY(ensure(c, c->cub_tmp, tmp));
+            tmp = c->cub_tmp.cap;
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, hi_a, hi_b, lo_a, lo_b, k, 0, b, c->stream));
+            GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, lo_b, lo_a, hi_b, hi_a, k, 0, b, c->stream));
+            c->stats.lib_launches += 2 * (2 + (b + 7) / 8);
+            auto joined = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), JoinKey{lo_a, hi_a, b});
+            size_t tmp2 = 0;
+            GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp2, joined, part, d_nsel, k, c->stream));
+            GC_TRY(ensure(c, c->cub_tmp, tmp2));
+            tmp2 = c->cub_tmp.cap;
+            GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp2, joined, part, d_nsel, k, c->stream));
+            c->stats.lib_launches += 2;
+            GC_TRY(read_small(c, h, d_nsel, 8));
+            GC_TRY(sync(c));
+            mr = h[0];
+        }
+        if (!nccl && mr > 0)
+            GC_CUDA(c, cudaMemcpyAsync(c->canon.as<uint64_t>() + off, part, (size_t)mr * 8, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+        off += mr;
+        mine = mr;
+        GC_TRY(tm.end(r));
+    }
+    if (nccl) {
+        // sizes of every rank's part, then the parts (64-bit keys as int32 pairs)
+        uint32_t* share = reinterpret_cast<uint32_t*>(c->scal.as<char>() + 704);
+        *static_cast<uint32_t*>(c->hpin) = (uint32_t)mine;
+        GC_CUDA(c, cudaMemcpyAsync(share + c->rank, c->hpin, 4, cudaMemcpyHostToDevice, c->stream));
+        GC_TRY(allgather_u32(c, share + c->rank, share, 1));
+        GC_TRY(read_small(c, h, share, (size_t)P * 4));
+        GC_TRY(sync(c));
+        int64_t counts[64], offs[64];
+        off = 0;
+        for (int r = 0; r < P; ++r) {
+            counts[r] = 2 * (int64_t)reinterpret_cast<uint32_t*>(h)[r];
+            offs[r] = off;
+            off += counts[r];
+        }
+        if (mine > 0)
+            GC_CUDA(c, cudaMemcpyAsync(c->canon.as<int32_t>() + offs[c->rank], part, (size_t)mine * 8,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        GC_TRY(allgatherv_i32(c, c->canon.as<int32_t>(), c->canon.as<int32_t>(), counts, offs));
+        off /= 2;
+    }
+    *m_out = off;
+    return GC_OK;
+}
+
+// a4 across owners: DAG rows of the tails in each owner's rank range
+static int part_orient(gc_ctx* c, int64_t n, int b, int64_t m) {
+    const int P = build_owners(c);
+    const bool nccl = c->nccl != nullptr;
+    const int r0 = nccl ? c->rank : 0, r1 = nccl ? c->rank + 1 : P;
+    GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+    unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
+    int64_t* dptr = c->dag_ptr.as<int64_t>();
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
+    if (m > 0) GC_LAUNCH(c, k_tail_count, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b,
+                         c->rank_of.as<int32_t>(), cnt);
     size_t tmp = 0;
-    GC_CUDA(c, cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys_in, keys_out, (int)N, (int)n, ptr, ptr + 1,
-                                                  c->stream));
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, dptr, n + 1, c->stream));
     GC_TRY(ensure(c, c->cub_tmp, tmp));
     tmp = c->cub_tmp.cap;
-    GC_CUDA(c, cub::DeviceSegmentedSort::SortKeys(c->cub_tmp.p, tmp, keys_in, keys_out, (int)N, (int)n, ptr, ptr + 1,
-                                                  c->stream));
-    c->stats.lib_launches += 4;   // partition + small / medium + large segment kernels (estimate)
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cnt, dptr, n + 1, c->stream));
+    c->stats.lib_launches += 2;
+    int64_t cut[65], base[65];
+    GC_TRY(owner_cuts(c, dptr, n, P, cut, base));
+    int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 968);
+    int64_t* h = static_cast<int64_t*>(c->hpin);
+    int32_t* sel = c->vals_a.as<int32_t>();
+    uint64_t* ka = c->keys_a.as<uint64_t>();
+    uint64_t* kb = c->keys_b.as<uint64_t>();
+    OwnerTimer tm(c);
+    for (int r = r0; r < r1; ++r) {
+        const int64_t k = base[r + 1] - base[r];
+        if (k <= 0) continue;
+        GC_TRY(tm.begin(r));
+        GC_TRY(select_iota(c, m, TailInRange{c->canon.as<uint64_t>(), c->rank_of.as<int32_t>(), b, (uint32_t)cut[r],
+                                              (uint32_t)cut[r + 1]},
+                           sel, d_nsel));
+        GC_LAUNCH(c, k_orient_sel, grid_for(k), kThreads, 0, c->canon.as<uint64_t>(), sel, k, b,
+                  c->rank_of.as<int32_t>(), ka);
+        GC_TRY(radix_sort(c, ka, kb, sel, c->dag_eid.as<int32_t>() + base[r], k, 2 * b));
+        GC_LAUNCH(c, k_split_keys, grid_for(k), kThreads, 0, kb, k, b, c->dag_col.as<int32_t>() + base[r],
+                  c->dag_src.as<int32_t>() + base[r]);
+        GC_TRY(tm.end(r));
+    }
+    (void)h;
+    if (nccl) {
+        int64_t counts[64], offs[64];
+        for (int r = 0; r < P; ++r) {
+            counts[r] = base[r + 1] - base[r];
+            offs[r] = base[r];
+        }
+        GC_TRY(allgatherv_i32(c, c->dag_col.as<int32_t>(), c->dag_col.as<int32_t>(), counts, offs));
+        GC_TRY(allgatherv_i32(c, c->dag_src.as<int32_t>(), c->dag_src.as<int32_t>(), counts, offs));
+        GC_TRY(allgatherv_i32(c, c->dag_eid.as<int32_t>(), c->dag_eid.as<int32_t>(), counts, offs));
+    }
+    return GC_OK;
+}
+
+// in-lists across owners: the in-edges of the heads in each owner's rank range
+static int part_inlists(gc_ctx* c, int64_t n, int b, int64_t m) {
+    const int P = build_owners(c);
+    const bool nccl = c->nccl != nullptr;
+    const int r0 = nccl ? c->rank : 0, r1 = nccl ? c->rank + 1 : P;
+    GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
+    unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
+    int64_t* iptr = c->in_ptr.as<int64_t>();
+    GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
+    if (m > 0) GC_LAUNCH(c, k_head_count, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), m, cnt);
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, iptr, n + 1, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cnt, iptr, n + 1, c->stream));
+    c->stats.lib_launches += 2;
+    int64_t cut[65], base[65];
+    GC_TRY(owner_cuts(c, iptr, n, P, cut, base));
+    int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 968);
+    int32_t* sel = c->vals_a.as<int32_t>();
+    uint32_t* heads = reinterpret_cast<uint32_t*>(c->keys_a.p);
+    OwnerTimer tm(c);
+    for (int r = r0; r < r1; ++r) {
+        const int64_t k = base[r + 1] - base[r];
+        if (k <= 0) continue;
+        GC_TRY(tm.begin(r));
+        // positions ascending (stable selection), then a stable sort on the head: (head, tail) order
+        GC_TRY(select_iota(c, m, HeadInRange{c->dag_col.as<int32_t>(), (int32_t)cut[r], (int32_t)cut[r + 1]}, sel,
+                           d_nsel));
+        GC_LAUNCH(c, k_gather_heads, grid_for(k), kThreads, 0, sel, k, c->dag_col.as<int32_t>(), heads);
+        size_t t2 = 0;
+        uint32_t* hout = reinterpret_cast<uint32_t*>(c->in_dst.as<int32_t>() + base[r]);
+        int32_t* pout = c->in_pos.as<int32_t>() + base[r];
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, t2, heads, hout, sel, pout, k, 0, b, c->stream));
+        GC_TRY(ensure(c, c->cub_tmp, t2));
+        t2 = c->cub_tmp.cap;
+        GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, t2, heads, hout, sel, pout, k, 0, b, c->stream));
+        c->stats.lib_launches += 2 + (b + 7) / 8;
+        GC_LAUNCH(c, k_in_tail, grid_for(k), kThreads, 0, pout, k, c->dag_src.as<int32_t>(),
+                  c->in_src.as<int32_t>() + base[r]);
+        GC_TRY(tm.end(r));
+    }
+    if (nccl) {
+        int64_t counts[64], offs[64];
+        for (int r = 0; r < P; ++r) {
+            counts[r] = base[r + 1] - base[r];
+            offs[r] = base[r];
+        }
+        GC_TRY(allgatherv_i32(c, c->in_pos.as<int32_t>(), c->in_pos.as<int32_t>(), counts, offs));
+        GC_TRY(allgatherv_i32(c, c->in_src.as<int32_t>(), c->in_src.as<int32_t>(), counts, offs));
+        GC_TRY(allgatherv_i32(c, c->in_dst.as<int32_t>(), c->in_dst.as<int32_t>(), counts, offs));
+    }
     return GC_OK;
 }
 
@@ -428,7 +676,6 @@ int build_csr(gc_ctx* c) {
     c->n = 0;
     c->m = 0;
     c->bits = 1;
-    c->build_v2_done = false;
     GC_TRY(ensure(c, c->scal, 1024));
     int* d_scal = c->scal.as<int>();
     GC_TRY(host_scratch(c, 4096));
@@ -454,45 +701,18 @@ int build_csr(gc_ctx* c) {
 
     // ---- a2: pack, sort, unique
     int64_t m = 0;
-    if (nnz > 0) {
+    const bool part = part_build(c) && b <= 31;
+    for (int r = 0; r < 16; ++r) c->stats.part_build_ms[r] = 0.0;
+    if (nnz > 0 && part) {
+        GC_TRY(ensure(c, c->keys_a, (size_t)nnz * 8));
+        GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
+        GC_TRY(part_canonical(c, nnz, n, b, &m));
+    } else if (nnz > 0) {
         GC_TRY(ensure(c, c->keys_a, (size_t)nnz * 8));
         GC_TRY(ensure(c, c->keys_b, (size_t)nnz * 8));
         const uint64_t sent = (2 * b >= 64) ? ~0ULL : ((1ULL << (2 * b)) - 1);
         bool joined_done = false;
-        if (c->build_mode == 1 && b <= 31 && n <= ((int64_t)1 << 31) - 2) {
-            // bucket the raw pairs by their low endpoint, sort each bucket, unique
-            GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
-            GC_TRY(ensure(c, c->tmp_b, (size_t)(n + 1) * 8));
-            unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
-            int64_t* ptr = c->tmp_b.as<int64_t>();
-            GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
-            GC_LAUNCH(c, k_count_lo, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(), nnz,
-                      cnt);
-            GC_TRY(scan_counts(c, cnt, n, ptr));
-            GC_TRY(read_small(c, h, ptr + n, 8));
-            GC_TRY(sync(c));
-            const int64_t nv = h[0];                        // pairs that are no self loop
-            if (nv > 0) {
-                GC_LAUNCH(c, k_scatter_lo, grid_for(nnz), kThreads, 0, c->raw_u.as<int32_t>(), c->raw_v.as<int32_t>(),
-                          nnz, b, ptr, cnt, c->keys_a.as<uint64_t>());
-                GC_TRY(seg_sort<uint64_t>(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), nv, n, ptr));
-                GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
-                int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
-                size_t tmp2 = 0;
-                GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp2, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
-                                                     d_nsel, nv, c->stream));
-                GC_TRY(ensure(c, c->cub_tmp, tmp2));
-                tmp2 = c->cub_tmp.cap;
-                GC_CUDA(c, cub::DeviceSelect::Unique(c->cub_tmp.p, tmp2, c->keys_b.as<uint64_t>(),
-                                                     c->canon.as<uint64_t>(), d_nsel, nv, c->stream));
-                c->stats.lib_launches += 2;
-                GC_TRY(read_small(c, h, d_nsel, 8));
-                GC_TRY(sync(c));
-                m = h[0];
-            }
-            joined_done = true;
-            c->build_v2_done = true;
-        } else if (GC_SPLIT_SORT1 && b <= 31) {
+        if (GC_SPLIT_SORT1 && b <= 31) {
             // (lo, hi) order by two stable 32-bit pair sorts, hi then lo: the same
             // bytes per pass as one 64-bit key sort, with 32-bit digits passes
             uint32_t* lo_a = reinterpret_cast<uint32_t*>(c->keys_a.p);
@@ -529,9 +749,7 @@ int build_csr(gc_ctx* c) {
         }
         GC_TRY(ensure(c, c->canon, (size_t)nnz * 8));
         int64_t* d_nsel = reinterpret_cast<int64_t*>(d_scal + 8);
-        if (c->build_v2_done) {
-            // m known, no self-loop sentinel in the list
-        } else if (!joined_done) {
+        if (!joined_done) {
             size_t tmp = 0;
             GC_CUDA(c, cub::DeviceSelect::Unique(nullptr, tmp, c->keys_b.as<uint64_t>(), c->canon.as<uint64_t>(),
                                                  d_nsel, nnz, c->stream));
@@ -541,7 +759,6 @@ int build_csr(gc_ctx* c) {
                                                  c->canon.as<uint64_t>(), d_nsel, nnz, c->stream));
             c->stats.lib_launches += 2;
         }
-        if (!c->build_v2_done) {
         GC_TRY(read_small(c, h, d_nsel, 8));
         GC_TRY(sync(c));
         int64_t nsel = h[0];
@@ -549,7 +766,6 @@ int build_csr(gc_ctx* c) {
             GC_TRY(read_small(c, h + 1, c->canon.as<uint64_t>() + nsel - 1, 8));
             GC_TRY(sync(c));
             m = nsel - ((uint64_t)h[1] == sent ? 1 : 0);
-        }
         }
     }
     if (m >= ((int64_t)1 << 31) - 1) return fail(c, GC_ERR_RANGE, "gc_build_csr: m >= 2^31 (edge ids are int32)");
@@ -603,45 +819,17 @@ int build_csr(gc_ctx* c) {
         c->stats.lib_launches += 2 + (dbits + 7) / 8;
         GC_LAUNCH(c, k_rank_scatter, grid_for(n), kThreads, 0, ids_out, n, c->rank_of.as<int32_t>());
     }
-    if (c->build_mode == 1) {
-        // DAG rows: out-degree histogram, scan, scatter (head, id) into the
-        // tail's row, sort each row by head.  In-lists: in-degree histogram,
-        // scan, scatter the DAG position into the head's segment, sort each
-        // segment (DAG positions ascend with the tail).
-        GC_TRY(ensure(c, c->tmp_a, (size_t)(n + 1) * 8));
-        unsigned long long* cnt = c->tmp_a.as<unsigned long long>();
-        int64_t* dptr = c->dag_ptr.as<int64_t>();
-        int64_t* iptr = c->in_ptr.as<int64_t>();
-        GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
-        if (m > 0)
-            GC_LAUNCH(c, k_orient_count, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b,
-                      c->rank_of.as<int32_t>(), cnt);
-        GC_TRY(scan_counts(c, cnt, n, dptr));
-        if (m > 0) {
-            GC_LAUNCH(c, k_orient_scatter, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b,
-                      c->rank_of.as<int32_t>(), dptr, cnt, c->keys_a.as<uint64_t>(), c->dag_src.as<int32_t>());
-            GC_TRY(seg_sort<uint64_t>(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), m, n, dptr));
-            GC_LAUNCH(c, k_split_rows, grid_for(m), kThreads, 0, c->keys_b.as<uint64_t>(), m, c->dag_col.as<int32_t>(),
-                      c->dag_eid.as<int32_t>());
-        }
-        GC_CUDA(c, cudaMemsetAsync(cnt, 0, (size_t)(n + 1) * 8, c->stream));
-        if (m > 0) GC_LAUNCH(c, k_count_head, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), m, cnt);
-        GC_TRY(scan_counts(c, cnt, n, iptr));
-        if (m > 0) {
-            uint32_t* pos = reinterpret_cast<uint32_t*>(c->keys_a.p);
-            GC_LAUNCH(c, k_in_scatter, grid_for(m), kThreads, 0, c->dag_col.as<int32_t>(), m, iptr, cnt, pos);
-            GC_TRY(seg_sort<uint32_t>(c, pos, reinterpret_cast<uint32_t*>(c->in_pos.p), m, n, iptr));
-            GC_LAUNCH(c, k_in_fill, grid_for(m), kThreads, 0, c->in_pos.as<int32_t>(), m, c->dag_src.as<int32_t>(),
-                      c->dag_col.as<int32_t>(), c->in_src.as<int32_t>(), c->in_dst.as<int32_t>());
-        }
+    if (part) {
+        GC_TRY(part_orient(c, n, b, m));
+        GC_TRY(part_inlists(c, n, b, m));
     }
-    if (m > 0 && c->build_mode != 1) {
+    if (m > 0 && !part) {
         GC_LAUNCH(c, k_orient, grid_for(m), kThreads, 0, c->canon.as<uint64_t>(), m, b, c->rank_of.as<int32_t>(),
                   c->keys_a.as<uint64_t>(), c->vals_a.as<int32_t>());
         GC_TRY(radix_sort(c, c->keys_a.as<uint64_t>(), c->keys_b.as<uint64_t>(), c->vals_a.as<int32_t>(),
                           c->dag_eid.as<int32_t>(), m, 2 * b));
     }
-    if (c->build_mode != 1) {
+    if (!part) {
         // split the sorted keys into (dag_col, dag_src) and the row bounds in one pass;
         // keys_a is free after the sort: first / last there, row lengths in vals_a
         int32_t* first = reinterpret_cast<int32_t*>(c->keys_a.p);
@@ -654,8 +842,8 @@ int build_csr(gc_ctx* c) {
         GC_TRY(ptr_from_bounds(c, first, last, n, c->tmp_a.as<int64_t>(), c->dag_ptr.as<int64_t>()));
     }
     // in-lists: sort (head, tail) with the DAG position as payload
-    if (c->build_mode == 1) {
-        // built above
+    if (part) {
+        // built by part_inlists
     } else if (m > 0) {
         // DAG order is sorted by (tail, head): a stable sort on the head alone
         // (b-bit keys, 32-bit) groups in-edges by head with tails ascending.

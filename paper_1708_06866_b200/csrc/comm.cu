@@ -8,7 +8,10 @@
 //   edge support    ncclAllReduce(uint32, sum, m)
 //   k-truss peel    ncclAllGather of the removed-edge bitmap (per round; at a
 //                   level start also the zero-support bitmap and an
-//                   ncclAllReduce(min) of the smallest support left out)
+//                   ncclAllReduce(min) of the smallest support left out);
+//                   per chunk of a round's owned frontier, the decrements of
+//                   other ranks' edges: counts by ncclAllGather, lists by
+//                   grouped ncclBroadcast (allgatherv_i32)
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -27,6 +30,9 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     bool ok = false;
     std::string why;
@@ -58,6 +64,9 @@ NcclApi& api() {
     SYM(CommAbort, "ncclCommAbort");
     SYM(AllReduce, "ncclAllReduce");
     SYM(AllGather, "ncclAllGather");
+    SYM(Broadcast, "ncclBroadcast");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
     A.ok = true;
@@ -127,9 +136,37 @@ int allreduce_min_u32(gc_ctx* c, uint32_t* dev, size_t count) {
     return GC_OK;
 }
 
+int allreduce_max_u32(gc_ctx* c, uint32_t* dev, size_t count) {
+    ncclResult_t r = api().AllReduce(dev, dev, count, ncclUint32, ncclMax, static_cast<ncclComm_t>(c->nccl), c->stream);
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllReduce(u32, max)");
+    return GC_OK;
+}
+
 int allgather_u32(gc_ctx* c, const uint32_t* send, uint32_t* recv, size_t count_per_rank) {
     ncclResult_t r = api().AllGather(send, recv, count_per_rank, ncclUint32, static_cast<ncclComm_t>(c->nccl), c->stream);
     if (r != ncclSuccess) return nccl_fail(c, r, "ncclAllGather(u32)");
+    return GC_OK;
+}
+
+// Variable-size allgather of int32 lists: rank r's counts[r] entries at
+// send land at recv + offsets[r] on every rank (one ncclBroadcast per root,
+// fused in a group).  counts / offsets are host arrays of nranks entries.
+int allgatherv_i32(gc_ctx* c, const int32_t* send, int32_t* recv, const int64_t* counts, const int64_t* offsets) {
+    NcclApi& A = api();
+    ncclComm_t comm = static_cast<ncclComm_t>(c->nccl);
+    ncclResult_t r = A.GroupStart();
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclGroupStart");
+    for (int root = 0; root < c->nranks; ++root) {
+        if (counts[root] == 0) continue;
+        r = A.Broadcast(root == c->rank ? send : recv + offsets[root], recv + offsets[root], (size_t)counts[root],
+                        ncclInt32, root, comm, c->stream);
+        if (r != ncclSuccess) {
+            A.GroupEnd();
+            return nccl_fail(c, r, "ncclBroadcast");
+        }
+    }
+    r = A.GroupEnd();
+    if (r != ncclSuccess) return nccl_fail(c, r, "ncclGroupEnd");
     return GC_OK;
 }
 

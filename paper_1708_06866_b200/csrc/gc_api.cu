@@ -247,13 +247,15 @@ int gc_destroy(gc_ctx* c) {
                         &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->front_a,
                         &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->zbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist,
-                        &c->vdeg, &c->zlist};
+                        &c->vdeg, &c->zlist, &c->task_pref, &c->dec_out, &c->dec_in};
     for (auto* b : bufs) release(c, *b);
     cudaStreamSynchronize(c->stream);
     if (c->pool) cudaMemPoolDestroy(c->pool);   // returns the cached blocks to the device
     nccl_destroy(c);
     if (c->hpin) cudaFreeHost(c->hpin);
     for (auto& ev : c->ev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->pev)
         if (ev) cudaEventDestroy(ev);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->copy_s) cudaStreamDestroy(c->copy_s);
@@ -557,9 +559,9 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
         case GC_OPT_PEEL_PART:
             c->peel_part = value ? 1 : 0;
             return GC_OK;
-        case GC_OPT_BUILD:
-            if (value < 0 || value > 1) return fail(c, GC_ERR_INVALID, "build mode must be 0 or 1");
-            c->build_mode = (int)value;
+        case GC_OPT_BUILD_PART:
+            if (value < -1 || value > 1) return fail(c, GC_ERR_INVALID, "build partition mode must be -1, 0 or 1");
+            c->build_part = (int)value;
             return GC_OK;
         case GC_OPT_WORK_STATS:
             c->work_stats = value ? 1 : 0;

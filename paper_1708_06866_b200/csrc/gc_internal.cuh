@@ -69,8 +69,7 @@ struct gc_ctx {
 
     // options
     int force_class = -1;
-    int build_mode = 0;              // GC_OPT_BUILD: 1 counting-sort build (bucket + segmented sort), 0 global radix sorts
-    bool build_v2_done = false;      // the last build's canonicalisation took the counting-sort path
+    int build_part = -1;             // GC_OPT_BUILD_PART: -1 auto (partitioned build when parts > 1), 0 replicated, 1 partitioned
     int64_t task_chunk = 32768;
     int timing = 1;
     int block_bitmap = 1;
@@ -118,6 +117,8 @@ struct gc_ctx {
     int64_t ntask[4] = {0, 0, 0, 0};
     int64_t task_off[5] = {0, 0, 0, 0, 0};
     int64_t total_cost = 0;
+    gcx::Buf task_pref;     // int64 exclusive cost prefix over the class-sorted tasks (multi-owner cut)
+    int64_t cls_start[4] = {0, 0, 0, 0}, cls_total[4] = {1, 1, 1, 1};
     int task_parts = 1;     // number of owners the tasks were cut for
     bool tasks_ready = false;
 
@@ -162,6 +163,7 @@ struct gc_ctx {
     gcx::Buf xbits;     // uint32 removed-edge bitmap X of the round (partitioned peel, allgathered)
     gcx::Buf nbits;     // uint32 next-round bitmap (each owner sets bits in its slice)
     gcx::Buf zbits;     // uint32 zero-support edges of a level start (removed without enumeration)
+    gcx::Buf dec_out, dec_in;   // partitioned peel (NCCL): decrements of other ranks' edges, sent / received
     gcx::Buf sup_parts; // uint32[P*m] per-virtual-rank supports (loopback partitions only)
     int peel_part = 0;  // 1: partitioned (bitmap) peeler even on one rank (GC_OPT_PEEL_PART)
     int work_stats = 0; // GC_OPT_WORK_STATS: count the k-truss byte model's terms while peeling
@@ -175,6 +177,7 @@ struct gc_ctx {
 
     // events
     cudaEvent_t ev[14] = {};   // 0-7 phases; 8-13 peel sub-phases (kernel / scan / compaction)
+    cudaEvent_t pev[17] = {};  // loopback partitions: per virtual rank intersection time (created on first use)
 
     gc_stats stats = {};
 
@@ -230,7 +233,9 @@ int nccl_destroy(gc_ctx* c);
 int allreduce_u64(gc_ctx* c, uint64_t* dev, size_t count);
 int allreduce_u32(gc_ctx* c, uint32_t* dev, size_t count);
 int allreduce_min_u32(gc_ctx* c, uint32_t* dev, size_t count);
+int allreduce_max_u32(gc_ctx* c, uint32_t* dev, size_t count);
 int allgather_u32(gc_ctx* c, const uint32_t* send, uint32_t* recv, size_t count_per_rank);
+int allgatherv_i32(gc_ctx* c, const int32_t* send, int32_t* recv, const int64_t* counts, const int64_t* offsets);
 
 inline int ceil_log2_u64(uint64_t x) {  // bits needed to represent values < x (x >= 1)
     int b = 0;

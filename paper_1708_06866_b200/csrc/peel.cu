@@ -263,17 +263,34 @@ struct PolicySingle {       // one rank: X = {st == st_front(round)}; crossings 
     }
 };
 
-struct PolicyPart {         // P ranks: X as a bitmap; only owned edges [lo, hi) are decremented
+// P owners of contiguous, word-aligned DAG-position slices (§8(e); the
+// enumeration partitioned by owner, §8(f) #1 "v2"): X travels as a bitmap,
+// each X edge is enumerated by its owner only (its S is exact there: early
+// exit), and a decrement lands on the survivor's owner copy -- directly for
+// loopback virtual ranks (one device), through a list exchanged after the
+// chunk for another NCCL rank.
+struct PolicyPart {
     const uint32_t* xbits;
-    uint32_t* S;
+    uint32_t* S;            // owner copies: owner o's at S + o * stride (loopback: stride m; NCCL: own copy, stride 0)
+    int64_t stride;
+    int64_t span;           // edges per owner slice (32 W)
+    int me;                 // NCCL: this rank; -1: loopback (every owner on this device)
     uint32_t thr;
-    int64_t lo, hi;
-    uint32_t* nbits;
-    // S(e) is exact only for owned e (an upper bound otherwise)
-    __device__ __forceinline__ uint32_t live(int e) const { return (e >= lo && e < hi) ? S[e] : 0xFFFFFFFFu; }
+    uint32_t* nbits;        // next X: crossings set their bit (owner's slice)
+    int32_t* out;           // NCCL: decrements of other ranks' edges
+    unsigned long long* out_n;
+    int64_t out_cap;
+    __device__ __forceinline__ int owner(int64_t e) const { return (int)(e / span); }
+    __device__ __forceinline__ uint32_t live(int e) const { return S[(int64_t)owner(e) * stride + e]; }
     __device__ __forceinline__ bool in_x(int f) const { return (xbits[f >> 5] >> (f & 31)) & 1u; }
     __device__ __forceinline__ void dec(int f) const {
-        if (f >= lo && f < hi && atomicSub(S + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
+        const int o = owner(f);
+        if (me < 0 || o == me) {
+            if (atomicSub(S + (int64_t)o * stride + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
+        } else {
+            const unsigned long long i = atomicAdd(out_n, 1ULL);
+            if ((int64_t)i < out_cap) out[i] = f;
+        }
     }
 };
 
@@ -694,6 +711,26 @@ __global__ void k_bits_to_list(const uint32_t* __restrict__ bits, int64_t nwords
     }
 }
 
+// list entries (indices within a slice) += the slice's first edge
+__global__ void k_offset_list(int32_t* __restrict__ list, const int* __restrict__ n_dev, int32_t off) {
+    const int n = *n_dev;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) list[i] += off;
+}
+
+__global__ void k_u64_to_u32(const unsigned long long* __restrict__ a, uint32_t* __restrict__ b) {
+    if (threadIdx.x == 0) *b = (uint32_t)*a;
+}
+
+// received decrements (NCCL partitioned peel): apply those of this rank's
+// edges [lo, hi) to its support copy; a crossing sets the next X bit
+__global__ void k_apply_decrements(const int32_t* __restrict__ in, int64_t n, int64_t lo, int64_t hi,
+                                   uint32_t* __restrict__ S, uint32_t thr, uint32_t* __restrict__ nbits) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int f = in[i];
+        if (f >= lo && f < hi && atomicSub(S + f, 1u) == thr) atomicOr(nbits + (f >> 5), 1u << (f & 31));
+    }
+}
+
 __global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, uint8_t* __restrict__ alive,
                                int32_t* __restrict__ tau, int32_t level) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
@@ -1109,6 +1146,102 @@ static uint32_t* part_support(gc_ctx* c, int r) {
     return c->sup.as<uint32_t>();
 }
 
+// NCCL rounds of the partitioned peel (host-driven).  Per round: this
+// rank's slice of the gathered X is its frontier; it is cut into chunks of at
+// most K edges so a chunk's decrements of other ranks' edges fit the send
+// list (an X edge has S < thr, so it destroys fewer than thr triangles:
+// at most 2 (thr - 1) decrements); the chunk count is the ranks' maximum
+// (every rank issues the same collectives).  Per chunk: enumerate, allgather
+// the list sizes, allgatherv the lists, apply the received ones this rank
+// owns.  Then every rank removes the whole X and the next X is allgathered.
+static int peel_rounds_nccl(gc_ctx* c, uint32_t thr, int32_t level, int nf, int64_t* removed, uint32_t* xb,
+                            uint32_t* nb) {
+    const int64_t m = c->m;
+    const int P = c->nranks, me = c->rank;
+    const int64_t W = part_words(c, P);
+    const int64_t lo = std::min<int64_t>(m, (int64_t)me * W * 32), hi = std::min<int64_t>(m, (int64_t)(me + 1) * W * 32);
+    int* cnt = reinterpret_cast<int*>(c->scal.as<char>() + 224);
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 256);
+    unsigned long long* out_n = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 696);
+    uint32_t* share = reinterpret_cast<uint32_t*>(c->scal.as<char>() + 704);   // P <= 64 u32 (704..960)
+    int32_t* h = static_cast<int32_t*>(c->hpin);
+    int32_t* own = c->front_a.as<int32_t>();
+    int32_t* all = c->front_b.as<int32_t>();
+    int32_t* tau = level >= 0 ? c->tau.as<int32_t>() : nullptr;
+    const int64_t cap = std::max<int64_t>(1 << 20, std::min<int64_t>(m, (int64_t)1 << 26));
+    GC_TRY(ensure(c, c->dec_out, (size_t)cap * 4));
+    GC_TRY(ensure(c, c->dec_in, (size_t)cap * P * 4));
+    const int64_t K = std::max<int64_t>(1, cap / (2 * (int64_t)std::max<uint32_t>(thr, 1)));
+    const int64_t z = *removed, alive0 = c->m_alive_h;
+    unsigned long long done[2] = {0, 0};
+    while (nf > 0) {
+        GC_TRY(record(c, 8));
+        GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
+        // own frontier, and the largest one over the ranks
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
+        GC_LAUNCH(c, k_bits_to_list, grid_for(W), kThreads, 0, xb + (size_t)me * W, W, own, cnt);
+        GC_LAUNCH(c, k_offset_list, grid_for(W * 32), kThreads, 0, own, cnt, (int32_t)(me * W * 32));
+        GC_CUDA(c, cudaMemcpyAsync(share, cnt, 4, cudaMemcpyDeviceToDevice, c->stream));
+        GC_TRY(allreduce_max_u32(c, share, 1));
+        GC_TRY(read_small(c, h, cnt, 4));
+        GC_TRY(read_small(c, h + 1, share, 4));
+        GC_TRY(sync(c));
+        const int64_t n_own = h[0], n_max = (uint32_t)h[1];
+        const int64_t chunks = (n_max + K - 1) / K;
+        for (int64_t ch = 0; ch < chunks; ++ch) {
+            const int64_t i0 = std::min(n_own, ch * K), i1 = std::min(n_own, (ch + 1) * K);
+            GC_CUDA(c, cudaMemsetAsync(out_n, 0, 8, c->stream));
+            if (i1 > i0) {
+                PolicyPart pol{xb, c->sup.as<uint32_t>(), 0, W * 32, me, thr, nb, c->dec_out.as<int32_t>(), out_n, cap};
+                PeelArgs A{own + i0, (int)(i1 - i0), nullptr, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                           c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                           c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
+                const int blocks = (int)std::min<int64_t>(((i1 - i0) * 32 + 255) / 256, 148 * 8);
+                GC_TRY(launch_peel(c, blocks, A, pol, i1 - i0));
+            }
+            // sizes of every rank's send list, then the lists
+            GC_LAUNCH(c, k_u64_to_u32, 1, 32, 0, out_n, share + me);
+            GC_TRY(allgather_u32(c, share + me, share, 1));
+            GC_TRY(read_small(c, h, share, (size_t)P * 4));
+            GC_TRY(read_small(c, h + 64, out_n, 8));
+            GC_TRY(sync(c));
+            if (*reinterpret_cast<uint64_t*>(h + 64) > (uint64_t)cap)
+                return fail(c, GC_ERR_RANGE, "partitioned peel: decrement list overflow");
+            int64_t counts[64], offs[64], tot = 0;
+            for (int r = 0; r < P; ++r) {
+                counts[r] = (uint32_t)h[r];
+                offs[r] = tot;
+                tot += counts[r];
+            }
+            if (tot > 0) {
+                GC_TRY(allgatherv_i32(c, c->dec_out.as<int32_t>(), c->dec_in.as<int32_t>(), counts, offs));
+                GC_LAUNCH(c, k_apply_decrements, grid_for(tot), kThreads, 0, c->dec_in.as<int32_t>(), tot, lo, hi,
+                          c->sup.as<uint32_t>(), thr, nb);
+            }
+        }
+        // every rank removes the whole X; the next X is gathered
+        GC_CUDA(c, cudaMemsetAsync(cnt + 1, 0, sizeof(int), c->stream));
+        GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, all, cnt + 1);
+        GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, all, cnt + 1, c->alive.as<uint8_t>(), tau, level, acc);
+        std::swap(xb, nb);
+        GC_TRY(allgather_u32(c, xb + (size_t)me * W, xb, (size_t)W));
+        GC_CUDA(c, cudaMemsetAsync(cnt, 0, sizeof(int), c->stream));
+        GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, all, cnt);
+        GC_TRY(record(c, 9));
+        GC_TRY(read_small(c, h, cnt, sizeof(int)));
+        GC_TRY(read_small(c, h + 2, acc, 16));
+        GC_TRY(sync(c));
+        c->stats.peel_kernel_ms += elapsed(c, 8, 9);
+        memcpy(done, h + 2, 16);
+        nf = h[0];
+        c->m_alive_h = alive0 - (int64_t)done[0];
+        if (nf > 0) GC_TRY(maybe_compact(c));
+    }
+    *removed = z + (int64_t)done[0];
+    c->stats.peel_rounds += (int64_t)done[1];
+    return GC_OK;
+}
+
 // One level of the partitioned peel.  At the level start each owner scans
 // its range into the frontier bitmap X and the zero-support bitmap Z; both
 // are allgathered, Z's edges leave on every rank without enumeration (they
@@ -1176,6 +1309,11 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         *next_thr = nf > 0 ? 0u : (mr == 0xFFFFFFFFu ? 0u : mr + 1);
     }
     if (nf > 0) GC_TRY(ensure_rows(c));
+    if (nccl) return peel_rounds_nccl(c, thr, level, nf, removed, xb, nb);
+    // Loopback virtual ranks (one device): every X edge is enumerated once,
+    // with its owner's support copy, and decrements land on the survivors'
+    // owner copies directly -- the v2 partition without the exchange.
+    // Rounds run in device-side batches like the single-rank peeler.
     const int64_t alive0 = c->m_alive_h;
     int cur = 0, batch = c->trace > 1 ? 1 : 2, last_nf = nf;
     unsigned long long done[2] = {0, 0};
@@ -1184,17 +1322,14 @@ static int peel_level_part(gc_ctx* c, uint32_t thr, int32_t level, int64_t* remo
         for (int b = 0; b < batch; ++b) {
             const int nxt = cur ^ 1;
             GC_CUDA(c, cudaMemsetAsync(nb, 0, (size_t)P * W * 4, c->stream));
-            for (int r = r_begin; r < r_end; ++r) {
-                PolicyPart pol{xb, part_support(c, r), thr, lo_of(r), hi_of(r), nb};
-                PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
-                           c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
-                           c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
-                GC_TRY(launch_peel(c, 148 * 8, A, pol, b == 0 ? (int64_t)nf : 0));
-            }
+            PolicyPart pol{xb, part_support(c, 0), c->loop_parts > 1 ? m : 0, W * 32, -1, thr, nb, nullptr, nullptr, 0};
+            PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+                       c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
+                       c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
+            GC_TRY(launch_peel(c, 148 * 8, A, pol, b == 0 ? (int64_t)nf : 0));
             GC_LAUNCH(c, k_finish_round_dev, 148 * 4, kThreads, 0, lists[cur], counts[cur], c->alive.as<uint8_t>(),
                       tau, level, acc);
             std::swap(xb, nb);
-            if (nccl) GC_TRY(allgather_u32(c, xb + (size_t)c->rank * W, xb, (size_t)W));
             GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
             GC_LAUNCH(c, k_bits_to_list, grid_for(P * W), kThreads, 0, xb, P * W, lists[nxt], counts[nxt]);
             cur = nxt;

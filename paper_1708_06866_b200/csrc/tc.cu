@@ -186,6 +186,15 @@ __global__ void k_task_flags(const int64_t* __restrict__ pref, const int32_t* __
     }
 }
 
+__global__ void k_task_cost(const uint64_t* __restrict__ packed, int64_t nt, const int64_t* __restrict__ in_cost,
+                            int64_t* __restrict__ cost) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nt; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t == nt) { cost[t] = 0; continue; }
+        const uint64_t pk = packed[t];
+        cost[t] = in_cost[(uint32_t)(pk >> 32)] - in_cost[(uint32_t)pk];
+    }
+}
+
 __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int64_t m,
                             const int32_t* __restrict__ in_dst, const int64_t* __restrict__ in_ptr,
                             const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col, int force,
@@ -401,6 +410,8 @@ struct KArgs {
     int64_t ntask;
     int64_t total_cost;
     int parts, owner;           // skip tasks not owned by `owner` of `parts`
+    const int64_t* task_pref;   // exclusive cost prefix over the tasks (this class's slice)
+    int64_t cls_start, cls_total;   // ... the class's first prefix value and its total cost
     uint32_t* sup;
     unsigned long long* count;
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
@@ -412,9 +423,14 @@ struct KArgs {
     long long* slot;            // ... and 2 slots per block publishing the next batch id to its warps
 };
 
-__device__ __forceinline__ bool owned(const KArgs& a, int i0) {
+// 1D cut per class: task t of a class belongs to owner
+// floor((cost of the class's tasks before t) * parts / class total), so every
+// owner gets 1/parts of every class's cost units.  (One cut over all classes
+// gave the owner of the lowest-ranked heads -- warp and lane tasks, dearer per
+// cost unit than block tasks -- 1.9x the mean TC time at 8 loopback parts.)
+__device__ __forceinline__ bool owned(const KArgs& a, int64_t t) {
     if (a.parts <= 1) return true;
-    return (int)((a.in_cost[i0] * a.parts) / a.total_cost) == a.owner;
+    return (int)(((a.task_pref[t] - a.cls_start) * a.parts) / a.cls_total) == a.owner;
 }
 
 __device__ __forceinline__ void add_count(unsigned long long* count, uint32_t hits, int lane) {
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(256, GC_TINY_MINB) k_tc_tiny(KArgs a) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < a.ntask; t += nt) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
-        if (!owned(a, i0)) continue;
+        if (!owned(a, t)) continue;
         const int v = __ldg(a.in_dst + i0);
         const int64_t r0 = __ldg(a.dag_ptr + v);
         const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
@@ -488,7 +504,7 @@ __global__ void __launch_bounds__(256, GC_WARP_MINB) k_tc_warp(KArgs a) {
     for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < a.ntask; t += nw) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
-        if (!owned(a, i0)) continue;
+        if (!owned(a, t)) continue;
         const int v = __ldg(a.in_dst + i0);
         const int64_t r0 = __ldg(a.dag_ptr + v);
         const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
@@ -671,7 +687,7 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     for (int64_t t = bt * a.batch; t < min(a.ntask, (bt + 1) * a.batch); ++t) {
         const uint64_t pk = a.tasks[t];
         const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
-        if (!owned(a, i0)) continue;
+        if (!owned(a, t)) continue;
         const int v = __ldg(a.in_dst + i0);
         if (v != cur) {
             __syncthreads();                      // every warp is done with cur's table
@@ -809,7 +825,7 @@ int prepare_tasks(gc_ctx* c) {
               c->dag_ptr.as<int64_t>(), c->dag_col.as<int32_t>(), c->n, c->task_chunk, c->force_class, bm_bits_of(c),
               hch);
     GC_LAUNCH(c, k_task_flags, grid_for(m), kThreads, 0, c->in_cost.as<int64_t>(), c->in_dst.as<int32_t>(),
-              c->in_ptr.as<int64_t>(), hch, m, c->total_cost, c->task_parts, flags);
+              c->in_ptr.as<int64_t>(), hch, m, c->total_cost, 1, flags);
     int32_t* sel = c->vals_a.as<int32_t>();
     int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 128);
     thrust::counting_iterator<int32_t> iota(0);
@@ -847,6 +863,27 @@ int prepare_tasks(gc_ctx* c) {
         off += h[k];
     }
     c->task_off[4] = off;
+    if (c->task_parts > 1 && nt > 0) {
+        // per-class 1D cut: exclusive cost prefix over the class-sorted tasks
+        GC_TRY(ensure(c, c->task_pref, (size_t)(nt + 1) * 8));
+        int64_t* tcost = c->tmp_a.as<int64_t>();           // free after the task build
+        GC_LAUNCH(c, k_task_cost, grid_for(nt + 1), kThreads, 0, c->task_i0.as<uint64_t>(), nt,
+                  c->in_cost.as<int64_t>(), tcost);
+        size_t tmp3 = 0;
+        GC_CUDA(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp3, tcost, c->task_pref.as<int64_t>(), nt + 1, c->stream));
+        GC_TRY(ensure(c, c->cub_tmp, tmp3));
+        tmp3 = c->cub_tmp.cap;
+        GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp3, tcost, c->task_pref.as<int64_t>(), nt + 1,
+                                                 c->stream));
+        c->stats.lib_launches += 2;
+        for (int k = 0; k <= 4; ++k)
+            GC_TRY(read_small(c, h + 8 + k, c->task_pref.as<int64_t>() + c->task_off[k], 8));
+        GC_TRY(sync(c));
+        for (int k = 0; k < 4; ++k) {
+            c->cls_start[k] = h[8 + k];
+            c->cls_total[k] = std::max<int64_t>(1, h[9 + k] - h[8 + k]);
+        }
+    }
     c->tasks_ready = true;
     return GC_OK;
 }
@@ -904,6 +941,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         a.slot = slots;
         a.tasks = tasks + c->task_off[3];
         a.ntask = c->ntask[3];
+        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[3] : nullptr;
+        a.cls_start = c->cls_start[3];
+        a.cls_total = c->cls_total[3];
         const size_t smem = (SUP ? 3 * kTS3 : kTS3) * sizeof(uint32_t);
         constexpr int threads = 32 * GC_HUGE_WARPS(SUP);
         const int grid = prep(3, k_tc_block<SUP, true>, smem, threads);
@@ -915,6 +955,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         a.slot = slots + 2 * 4096;
         a.tasks = tasks + c->task_off[2];
         a.ntask = c->ntask[2];
+        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[2] : nullptr;
+        a.cls_start = c->cls_start[2];
+        a.cls_total = c->cls_total[2];
         const size_t smem = (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
         constexpr int threads = 32 * (SUP ? GC_SUP_WARPS : GC_TC_WARPS);
         const int grid = prep(2, k_tc_block<SUP, false>, smem, threads);
@@ -924,6 +967,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[1] > 0) {
         a.tasks = tasks + c->task_off[1];
         a.ntask = c->ntask[1];
+        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[1] : nullptr;
+        a.cls_start = c->cls_start[1];
+        a.cls_total = c->cls_total[1];
         const size_t smem = kWarps * (SUP ? 3 * kTS1 : kTS1) * sizeof(uint32_t);
         const int grid = prep(1, k_tc_warp<kTS1, SUP>, smem, 256);
         if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_warp)", __FILE__, __LINE__);
@@ -933,6 +979,9 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     if (c->ntask[0] > 0) {
         a.tasks = tasks + c->task_off[0];
         a.ntask = c->ntask[0];
+        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[0] : nullptr;
+        a.cls_start = c->cls_start[0];
+        a.cls_total = c->cls_total[0];
         const int grid = prep(0, k_tc_tiny<SUP>, 0, 256);
         GC_LAUNCH_S(c, ws, (k_tc_tiny<SUP>), (int)std::min<int64_t>(grid, (a.ntask + 255) / 256), 256, 0, a);
     }
@@ -949,7 +998,26 @@ static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
     const int parts = c->task_parts;
     if (c->total_cost == 0) return GC_OK;
     if (c->loop_parts > 0) {
-        for (int r = 0; r < parts; ++r) GC_TRY(launch_classes<SUP>(c, r, parts, count, sup));
+        // per virtual rank device time (stats.part_ms): the balance of the 1D cut
+        const int nt = c->timing ? std::min(parts, 16) : 0;
+        for (int r = 0; r <= nt; ++r)
+            if (!c->pev[r]) GC_CUDA(c, cudaEventCreate(&c->pev[r]));
+        for (int r = 0; r < parts; ++r) {
+            if (r < nt) GC_CUDA(c, cudaEventRecord(c->pev[r], c->stream));
+            GC_TRY(launch_classes<SUP>(c, r, parts, count, sup));
+        }
+        if (nt > 0) {
+            GC_CUDA(c, cudaEventRecord(c->pev[nt], c->stream));
+            GC_CUDA(c, cudaEventSynchronize(c->pev[nt]));
+            for (int r = 0; r < 16; ++r) {
+                float ms = 0.f;
+                if (r < nt && cudaEventElapsedTime(&ms, c->pev[r], c->pev[r + 1]) != cudaSuccess) {
+                    cudaGetLastError();
+                    ms = 0.f;
+                }
+                c->stats.part_ms[r] = r < nt ? ms : 0.0;
+            }
+        }
     } else {
         GC_TRY(launch_classes<SUP>(c, c->rank, parts, count, sup));
     }

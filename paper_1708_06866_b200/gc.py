@@ -44,7 +44,7 @@ GC_OPT_GROUP_PEEL = 12
 GC_OPT_GROUP_HEAVY = 14
 GC_OPT_OVERLAP = 13
 GC_OPT_WORK_STATS = 15
-GC_OPT_BUILD = 16
+GC_OPT_BUILD_PART = 16
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -69,6 +69,7 @@ class gc_stats(ctypes.Structure):
         ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),
         ("aux", ctypes.c_int64 * 8),
         ("peel_sum_min", ctypes.c_int64), ("peel_decrements", ctypes.c_int64),
+        ("part_ms", ctypes.c_double * 16), ("part_build_ms", ctypes.c_double * 16),
     ]
 
 
@@ -332,6 +333,8 @@ class Context:
         out = {name: getattr(s, name) for name, _ in gc_stats._fields_}
         out["tasks"] = list(out["tasks"])
         out["aux"] = list(out["aux"])
+        out["part_ms"] = list(out["part_ms"])
+        out["part_build_ms"] = list(out["part_build_ms"])
         return out
 
     def reset_stats(self):

@@ -28,8 +28,12 @@ MUTANTS = {
     # O-5 merge branch
     "o5_merge_no_alive": ("else { if (alive[eid[i]] && alive[eid[j]]) ++c; ++i; ++j; }", "else { ++c; ++i; ++j; }"),
     "o5_threshold_off_by_one": ("(int64_t)s[e] < (int64_t)k - 2", "(int64_t)s[e] < (int64_t)k - 3"),
-    "o5_not_batch": ("if (alive[e] && (int64_t)s[e] < (int64_t)k - 2) { s[e] = 0xFFFFFFFFu; ++nx; }",
-                     "if (alive[e] && (int64_t)s[e] < (int64_t)k - 2) { alive[e] = 0; s[e] = 0xFFFFFFFFu; ++nx; }"),
+    "o5_x_stays_alive": ("                s[e] = 0xFFFFFFFFu;\n                ++nx;",
+                         "                ++nx;"),
+    "o5_work_min_not_max": ("work[0] += d[cu[e]] < d[cv[e]] ? d[cu[e]] : d[cv[e]];",
+                            "work[0] += d[cu[e]] > d[cv[e]] ? d[cu[e]] : d[cv[e]];"),
+    "o5_work_dec_sign": ("if (alive[e]) work[1] += (int64_t)prev[e] - (int64_t)s[e];",
+                         "if (alive[e]) work[1] += (int64_t)s[e] - (int64_t)prev[e];"),
     # O-3 intersection
     "o3_gallop_skip_candidate": ("lo = lower_bound32(B, lo, nb, A[i]);", "lo = lower_bound32(B, lo + 1, nb, A[i]);"),
     "o3_gallop_strict": ("if (lo < nb && B[lo] == A[i]) { ++c; ++lo; }", "if (lo + 1 < nb && B[lo] == A[i]) { ++c; ++lo; }"),

@@ -817,13 +817,17 @@ def test_nccl_one_rank_communicator(gcmod):
             assert c.stats()["peel_rounds"] > 0 or want_kmax <= 3
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_build_modes(gcmod, mode):
-    """Both gc_build_csr algorithms (GC_OPT_BUILD: 1 bucket + segmented sort,
-    0 global radix sorts) give the oracle's canonical list, supports and
-    k-trusses, on graphs with duplicates, reversed pairs, self loops, an
-    isolated top id, a hub, and the degenerate inputs."""
-    rng = np.random.default_rng(90 + mode)
+
+@pytest.mark.parametrize("setup", ["part1", "loop2", "loop3", "loop8", "nccl1"])
+def test_partitioned_build(gcmod, setup):
+    """gc_build_csr across owners (GC_OPT_BUILD_PART): each
+    owner sorts the raw pairs of its low-endpoint id range, the oriented edges
+    of its tail-rank range and the in-edges of its head-rank range; the parts
+    are concatenated (NCCL: grouped broadcasts).  One owner forced, loopback
+    2 / 3 / 8 virtual ranks, and a real one-rank NCCL communicator: canonical
+    list, supports, k-truss and decomposition equal the oracle's, on graphs
+    with duplicates, reversed pairs, self loops, a hub and degenerate inputs."""
+    rng = np.random.default_rng(90)
     hub_u = np.zeros(3000, np.int32)
     hub_v = rng.integers(1, 5000, 3000).astype(np.int32)
     cases = [gen.CONFIGS["C1"].generate(), gen.rmat(13, 16, seed=91), (hub_u, hub_v),
@@ -833,7 +837,11 @@ def test_build_modes(gcmod, mode):
     for u, v in cases:
         g = oracle.OracleGraph(u, v)
         with gcmod.Context(0) as c:
-            c.set_option(gcmod.GC_OPT_BUILD, mode)
+            if setup.startswith("loop"):
+                c.comm_init_loopback(int(setup[4:]))
+            elif setup == "nccl1":
+                c.comm_init(gcmod.nccl_unique_id(), 1, 0)
+            c.set_option(gcmod.GC_OPT_BUILD_PART, 1)
             c.load_edges(u, v)
             c.build_csr()
             assert (c.num_vertices(), c.num_edges()) == (g.n, g.m)
@@ -843,4 +851,6 @@ def test_build_modes(gcmod, mode):
             assert np.array_equal(c.edge_support(), g.support())
             want, _ = g.ktruss(4)
             assert np.array_equal(c.ktruss(4)[0], want)
-
+            tau, kmax = c.truss_decomposition()
+            want_tau, want_kmax = g.truss_decomposition()
+            assert np.array_equal(tau, want_tau) and kmax == want_kmax
