@@ -254,6 +254,9 @@ typedef enum gc_option {
                                  model's terms (gc_stats peel_sum_min,
                                  peel_decrements) at the cost of a few small kernels per
                                  round (default 0; measurement) */
+    GC_OPT_SORT_FRONT = 18,   /* peeler: a round whose frontier has at least this many edges
+                                 (known on the host) is first sorted by the endpoint whose live
+                                 row the per-edge search probes (0: never) */
     GC_OPT_BUILD_PART = 16,   /* gc_build_csr across owners: -1 (default)
                                  partitioned when there are several owners (NCCL ranks or
                                  loopback parts), 1 always (one owner included; testing),

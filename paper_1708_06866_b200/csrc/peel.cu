@@ -731,6 +731,18 @@ __global__ void k_apply_decrements(const int32_t* __restrict__ in, int64_t n, in
     }
 }
 
+// sort key of a frontier edge: its endpoint with the longer live row (the row
+// the per-edge search probes), so edges probing the same row run together
+__global__ void k_pivot_keys(const int32_t* __restrict__ front, int nf, const int32_t* __restrict__ dag_src,
+                             const int32_t* __restrict__ dag_col, const int32_t* __restrict__ live_len,
+                             uint32_t* __restrict__ keys) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+        const int e = front[i];
+        const int a = dag_src[e], b = dag_col[e];
+        keys[i] = (uint32_t)(live_len[a] > live_len[b] ? a : b);
+    }
+}
+
 __global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, uint8_t* __restrict__ alive,
                                int32_t* __restrict__ tau, int32_t level) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
@@ -973,6 +985,28 @@ static int peel_round_grouped(gc_ctx* c, const int32_t* front, int nf, const Pol
     return GC_OK;
 }
 
+// A big frontier (nf known on the host) sorted by the endpoint whose live row
+// the per-edge search probes (GC_OPT_SORT_FRONT): warps that search the same
+// hub row run close together and find its sectors in L2.
+static int sort_frontier(gc_ctx* c, int32_t* front, int nf) {
+    GC_TRY(ensure(c, c->grp_keys, (size_t)nf * 4 * 2));
+    GC_TRY(ensure(c, c->grp_vals, (size_t)nf * 4));
+    uint32_t* k0 = c->grp_keys.as<uint32_t>();
+    uint32_t* k1 = k0 + nf;
+    int32_t* v1 = c->grp_vals.as<int32_t>();
+    GC_LAUNCH(c, k_pivot_keys, grid_for(nf), kThreads, 0, front, nf, c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
+              c->live_len.as<int32_t>(), k0);
+    const int kbits = std::max(1, ceil_log2_u64((uint64_t)c->n));
+    size_t tmp = 0;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, front, v1, nf, 0, kbits, c->stream));
+    GC_TRY(ensure(c, c->cub_tmp, tmp));
+    tmp = c->cub_tmp.cap;
+    GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, k0, k1, front, v1, nf, 0, kbits, c->stream));
+    c->stats.lib_launches += 2 + (kbits + 7) / 8;
+    GC_CUDA(c, cudaMemcpyAsync(front, v1, (size_t)nf * 4, cudaMemcpyDeviceToDevice, c->stream));
+    return GC_OK;
+}
+
 // Work stats (GC_OPT_WORK_STATS): the edges of `gone` (count on the device)
 // leave the alive degrees, then the next round's frontier `next` adds its
 // min-degree term (either list may be null).
@@ -1096,6 +1130,7 @@ static int peel_level(gc_ctx* c, uint32_t thr, int32_t level, int32_t* round, in
             const int nxt = cur ^ 1;
             GC_CUDA(c, cudaMemsetAsync(counts[nxt], 0, sizeof(int), c->stream));
             PolicySingle pol{c->alive.as<uint8_t>(), c->sup.as<uint32_t>(), thr, *round, lists[nxt], counts[nxt]};
+            if (r == 0 && c->sort_front > 0 && nf >= c->sort_front) GC_TRY(sort_frontier(c, lists[cur], nf));
             PeelArgs A{lists[cur], 0, counts[cur], c->dag_src.as<int32_t>(), c->dag_col.as<int32_t>(),
                        c->sym_ptr.as<int64_t>(), c->live_len.as<int32_t>(), c->sym_col.as<int32_t>(),
                        c->sym_eid.as<int32_t>(), c->alive.as<uint8_t>()};
