@@ -256,7 +256,8 @@ typedef enum gc_option {
                                  round (default 0; measurement) */
     GC_OPT_SORT_FRONT = 18,   /* peeler: a round whose frontier has at least this many edges
                                  (known on the host) is first sorted by the endpoint whose live
-                                 row the per-edge search probes (0: never) */
+                                 row the per-edge search probes (default 2^20; 0: never;
+                                 C4 k = 4 / 6 peel -4 % / -5 %, decomposition -2 %) */
     GC_OPT_BUILD_PART = 16,   /* gc_build_csr across owners: -1 (default)
                                  partitioned when there are several owners (NCCL ranks or
                                  loopback parts), 1 always (one owner included; testing),

@@ -150,7 +150,7 @@ struct gc_ctx {
     int64_t peel_big = getenv("GC_PEEL_BIG") ? atoll(getenv("GC_PEEL_BIG")) : INT64_MAX;
     int group_peel = 0;         // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
     int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped
-    int sort_front = 0;         // GC_OPT_SORT_FRONT: frontiers of at least this many edges sorted by probed row (0: never)
+    int sort_front = 1 << 20;   // GC_OPT_SORT_FRONT: frontiers of at least this many edges sorted by probed row (0: never)
     gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)
     int64_t alist_n = -1;       // -1: no list (scan every edge)
     int64_t m_alive_h = 0;      // live edges (host mirror)
