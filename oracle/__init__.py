@@ -51,6 +51,9 @@ def _lib():
         L.or_truss_sequential.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p,
                                           i32p, u32p, i32p, i32p, ctypes.c_int]
         L.or_truss_sequential.restype = ctypes.c_int64
+        L.or_truss_parallel.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p, i32p, u32p,
+                                        i32p, i32p, ctypes.c_int]
+        L.or_truss_parallel.restype = ctypes.c_int64
         _LIB = L
     return _LIB
 
@@ -155,6 +158,26 @@ class OracleGraph:
                                        1 if consume else 0)
         if r < 0:
             raise MemoryError("or_truss_sequential: out of memory (or m > 2^31-1)")
+        if consume:
+            self.col = self.eid = None
+        return tau[: self.m].copy(), int(kmax.value)
+
+    # O-8
+    def truss_parallel(self, support: np.ndarray | None = None, consume: bool = False):
+        """O-8: Alg. 4's incremental update element-wise, rounds parallel over
+        the removed edges.  Uses the adjacency rows as scratch (copied unless
+        consume=True, which leaves this graph unusable)."""
+        if support is None:
+            support = self.support()
+        support = np.ascontiguousarray(support, dtype=np.uint32)
+        col, eid = (self.col, self.eid) if consume else (self.col.copy(), self.eid.copy())
+        tau = np.zeros(max(self.m, 1), dtype=np.int32)
+        kmax = ctypes.c_int32(0)
+        r = _lib().or_truss_parallel(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p), _p(self.ptr, i64p),
+                                     _p(col, i32p), _p(eid, i32p), _p(support, u32p), _p(tau, i32p),
+                                     ctypes.byref(kmax), self.nthreads)
+        if r < 0:
+            raise MemoryError("or_truss_parallel: out of memory (or m > 2^31-1)")
         if consume:
             self.col = self.eid = None
         return tau[: self.m].copy(), int(kmax.value)

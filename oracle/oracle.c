@@ -28,6 +28,9 @@
  *   O-7  or_truss_sequential  tier 2: one-edge-at-a-time min-support peel
  *                             (bucket order); equal to O-6 by uniqueness
  *                             of the maximal k-truss (reading A2/A8)
+ *   O-8  or_truss_parallel    tier 2: Alg. 4's incremental update
+ *                             element-wise, rounds in parallel
+ *                             over the edges of x; equal to O-6 and O-7
  *
  * Pins: tests/test_oracle_pins.py (brute force, closed forms, trace(A^3)/6,
  * literal Alg. 1-4 in scipy, networkx, Table II, invariants).
@@ -58,6 +61,33 @@ static void parallel_for(int64_t N, int T, range_fn fn, void* ctx) {
     for (int t = 0; t < T; ++t) {
         jb[t].fn = fn; jb[t].ctx = ctx; jb[t].i0 = N * t / T; jb[t].i1 = N * (t + 1) / T; jb[t].t = t;
         pthread_create(&th[t], NULL, range_tramp, &jb[t]);
+    }
+    for (int t = 0; t < T; ++t) pthread_join(th[t], NULL);
+    free(th); free(jb);
+}
+
+/* Run fn over [0, N) in chunks of `grain` taken from a shared counter by T
+ * threads (for uneven per-item work; results must not depend on who runs
+ * which chunk). */
+typedef struct { range_fn fn; void* ctx; int64_t N, grain; int64_t* next; int t; } dyn_job;
+static void* dyn_tramp(void* a) {
+    dyn_job* j = (dyn_job*)a;
+    for (;;) {
+        const int64_t i0 = __atomic_fetch_add(j->next, j->grain, __ATOMIC_RELAXED);
+        if (i0 >= j->N) break;
+        j->fn(j->ctx, i0, i0 + j->grain < j->N ? i0 + j->grain : j->N, j->t);
+    }
+    return NULL;
+}
+static void parallel_for_dynamic(int64_t N, int T, int64_t grain, range_fn fn, void* ctx) {
+    T = n_threads(T);
+    if (N <= grain || T == 1) { fn(ctx, 0, N, 0); return; }
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * T);
+    dyn_job* jb = (dyn_job*)malloc(sizeof(dyn_job) * T);
+    int64_t next = 0;
+    for (int t = 0; t < T; ++t) {
+        jb[t].fn = fn; jb[t].ctx = ctx; jb[t].N = N; jb[t].grain = grain; jb[t].next = &next; jb[t].t = t;
+        pthread_create(&th[t], NULL, dyn_tramp, &jb[t]);
     }
     for (int t = 0; t < T; ++t) pthread_join(th[t], NULL);
     free(th); free(jb);
@@ -512,4 +542,169 @@ int64_t or_truss_sequential(int64_t n, int64_t m, const int32_t* cu, const int32
     free(E); free(bin); free(ord); free(len); free(live); free(hits);
     if (!consume) { free(col); free(eid); }
     return ok ? m : -1;
+}
+
+/* ------------------------------------------------------------------ O-8 --
+ * Tier-2 decomposition, parallel: Alg. 4 with its incremental update
+ * written element-wise.  Levels k = 3, 4, ...;
+ * within a level, rounds: x = {alive e : s(e) < k-2} (batch, reading A4);
+ * every triangle alive at the round start with at least one edge in x loses
+ * those edges, so each of its surviving edges loses one unit of support --
+ * Alg. 4's R -= E_x-block update, counted once per triangle (reading A5: the
+ * triangle is handled by its smallest-id edge in x); the edges whose support
+ * falls below k-2 form the next round's x; x is removed with trussness k-1.
+ * A level whose first x would be empty is skipped (no support changes, so
+ * every k up to min s + 2 finds the same survivors).  Edges of x are handled
+ * by independent threads (static chunks; support decrements are atomic, so
+ * the result does not depend on the thread count or order).  The live
+ * triangles of e = (a,b) are N_live(a) ∩ N_live(b) by the same sorted-list
+ * intersection as O-3 / O-7; rows drop dead entries when the live edge count
+ * has halved.  Equal to O-6 and O-7 (uniqueness of the maximal k-truss);
+ * pinned against both.  sup_init: O-3 supports (m).  col/eid are used as row
+ * storage and left scrambled.  Returns the number of rounds, -1 on OOM. */
+typedef struct {
+    const int64_t* ptr; const int64_t* len; const int32_t* col; const int32_t* eid;
+    const int32_t* cu; const int32_t* cv; uint8_t* st; uint32_t* S; uint32_t thr;
+    const int32_t* x; int32_t* next; int64_t* nnext;
+} o8_round;
+
+static void o8_enumerate(void* c, int64_t i0, int64_t i1, int t) {
+    (void)t;
+    o8_round* R = (o8_round*)c;
+    for (int64_t i = i0; i < i1; ++i) {
+        const int32_t e = R->x[i];
+        const int32_t a = R->cu[e], b = R->cv[e];
+        int64_t p = R->ptr[a], p1 = R->ptr[a] + R->len[a], q = R->ptr[b], q1 = R->ptr[b] + R->len[b];
+        if (p1 - p > q1 - q) { int64_t s; s = p; p = q; q = s; s = p1; p1 = q1; q1 = s; }
+        const int gallop = (q1 - q) >= 32 * (p1 - p);
+        for (; p < p1 && q < q1; ++p) {
+            if (gallop) {
+                q = lower_bound32(R->col, q, q1, R->col[p]);
+                if (q >= q1) break;
+            } else {
+                while (q < q1 && R->col[q] < R->col[p]) ++q;
+                if (q >= q1) break;
+            }
+            if (R->col[q] != R->col[p]) continue;
+            const int32_t f = R->eid[p], g = R->eid[q];
+            ++q;
+            const uint8_t sf = R->st[f], sg = R->st[g];          /* 0 removed, 1 alive, 2 in x */
+            if (sf == 0 || sg == 0) continue;                     /* not a live triangle */
+            if ((sf == 2 && f < e) || (sg == 2 && g < e)) continue;   /* a smaller x edge handles it */
+            const int32_t fg[2] = {f, g};
+            const uint8_t sfg[2] = {sf, sg};
+            for (int k = 0; k < 2; ++k) {
+                if (sfg[k] != 1) continue;                        /* x edges are not decremented */
+                const uint32_t old = __atomic_fetch_sub(&R->S[fg[k]], 1u, __ATOMIC_RELAXED);
+                if (old == R->thr) {                              /* crossing: next round's x */
+                    const int64_t slot = __atomic_fetch_add(R->nnext, 1, __ATOMIC_RELAXED);
+                    R->next[slot] = fg[k];
+                }
+            }
+        }
+    }
+}
+
+/* level-start scan of the alive list, in T static chunks: chunk t keeps its
+ * alive edges (in place) and lists its x edges; counts per chunk */
+typedef struct {
+    int32_t* L; int64_t nL; const uint8_t* st; const uint32_t* S; uint32_t thr; int T;
+    int32_t* xbuf; int64_t* kept; int64_t* nx; uint32_t* smin;
+} o8_scan;
+static void o8_scan_chunk(void* c, int64_t t0, int64_t t1, int unused) {
+    (void)unused;
+    o8_scan* Q = (o8_scan*)c;
+    for (int64_t t = t0; t < t1; ++t) {
+        const int64_t i0 = Q->nL * t / Q->T, i1 = Q->nL * (t + 1) / Q->T;
+        int64_t w = i0, nx = 0;
+        uint32_t smin = 0xFFFFFFFFu;
+        for (int64_t i = i0; i < i1; ++i) {
+            const int32_t e = Q->L[i];
+            if (!Q->st[e]) continue;
+            Q->L[w++] = e;
+            if (Q->S[e] < Q->thr) Q->xbuf[i0 + nx++] = e;   /* within the chunk's own range */
+            else if (Q->S[e] < smin) smin = Q->S[e];
+        }
+        Q->kept[t] = w - i0;
+        Q->nx[t] = nx;
+        Q->smin[t] = smin;
+    }
+}
+
+typedef struct { const int64_t* ptr; int64_t* len; int32_t* col; int32_t* eid; const uint8_t* st; } o8_compact;
+static void o8_compact_rows(void* c, int64_t v0, int64_t v1, int t) {
+    (void)t;
+    o8_compact* C = (o8_compact*)c;
+    for (int64_t v = v0; v < v1; ++v) {
+        int64_t w = C->ptr[v];
+        for (int64_t r = C->ptr[v]; r < C->ptr[v] + C->len[v]; ++r)
+            if (C->st[C->eid[r]]) { C->col[w] = C->col[r]; C->eid[w] = C->eid[r]; ++w; }
+        C->len[v] = w - C->ptr[v];
+    }
+}
+
+int64_t or_truss_parallel(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv, const int64_t* ptr,
+                          int32_t* col, int32_t* eid, const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out,
+                          int nthreads) {
+    if (m == 0) { *kmax_out = 0; return 0; }
+    if (m > INT32_MAX) return -1;
+    const int T = n_threads(nthreads);
+    uint32_t* S = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)m);
+    uint8_t* st = (uint8_t*)malloc((size_t)m);
+    int32_t* L = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);      /* alive edges (compacted) */
+    int32_t* x = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+    int32_t* nx = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+    int64_t* len = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t* kept = (int64_t*)malloc(sizeof(int64_t) * (size_t)T);
+    int64_t* cnx = (int64_t*)malloc(sizeof(int64_t) * (size_t)T);
+    uint32_t* cmin = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)T);
+    if (!S || !st || !L || !x || !nx || !len || !kept || !cnx || !cmin) {
+        free(S); free(st); free(L); free(x); free(nx); free(len); free(kept); free(cnx); free(cmin);
+        return -1;
+    }
+    for (int64_t e = 0; e < m; ++e) { S[e] = sup_init[e]; st[e] = 1; L[e] = (int32_t)e; tau[e] = 2; }
+    for (int64_t v = 0; v < n; ++v) len[v] = ptr[v + 1] - ptr[v];
+    int64_t nL = m, alive = m, compact_at = m, rounds = 0;
+    int32_t kmax = 2;
+    for (int32_t k = 3; alive > 0; ++k) {
+        const uint32_t thr = (uint32_t)(k - 2);
+        /* the level's first x; min s over the rest (empty-level skip); L keeps the alive edges */
+        o8_scan Q = {L, nL, st, S, thr, T, nx, kept, cnx, cmin};
+        parallel_for(T, T, o8_scan_chunk, &Q);
+        int64_t w = 0, nxs = 0;
+        uint32_t smin = 0xFFFFFFFFu;
+        for (int t = 0; t < T; ++t) {
+            const int64_t i0 = nL * t / T;
+            memmove(L + w, L + i0, sizeof(int32_t) * (size_t)kept[t]);
+            memcpy(x + nxs, nx + i0, sizeof(int32_t) * (size_t)cnx[t]);
+            w += kept[t];
+            nxs += cnx[t];
+            if (cmin[t] < smin) smin = cmin[t];
+        }
+        nL = w;
+        if (nxs == 0) {
+            if (smin != 0xFFFFFFFFu && smin + 2 > (uint32_t)k) k = (int32_t)smin + 2;   /* loop's ++k: smin + 3 */
+            continue;
+        }
+        while (nxs > 0) {
+            for (int64_t i = 0; i < nxs; ++i) st[x[i]] = 2;
+            int64_t nn = 0;
+            o8_round R = {ptr, len, col, eid, cu, cv, st, S, thr, x, nx, &nn};
+            parallel_for_dynamic(nxs, T, 64, o8_enumerate, &R);
+            for (int64_t i = 0; i < nxs; ++i) { st[x[i]] = 0; tau[x[i]] = k - 1; }
+            if (k - 1 > kmax) kmax = k - 1;
+            alive -= nxs;
+            ++rounds;
+            int32_t* t = x; x = nx; nx = t;                        /* next round's x: the crossings */
+            nxs = nn;
+            if (alive > 0 && alive * 2 <= compact_at) {           /* rows drop their dead entries */
+                o8_compact C = {ptr, len, col, eid, st};
+                parallel_for(n, T, o8_compact_rows, &C);
+                compact_at = alive;
+            }
+        }
+    }
+    *kmax_out = kmax;
+    free(S); free(st); free(L); free(x); free(nx); free(len); free(kept); free(cnx); free(cmin);
+    return rounds;
 }

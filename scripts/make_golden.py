@@ -11,13 +11,17 @@ libgc's outputs with the files this script writes:
                                      for k = 3..6 derived as tau >= k
     tests/golden/c5_expected.json   the same for C5
 
+Trussness comes from O-7 (sequential bucket peel) or O-8 (Alg. 4's
+incremental rounds, parallel), or both with an equality check (--tau
+o7|o8|both; default o7 for C3/C4, o8 for C5, where O-7 would take ~10 h).
+
 Every per-edge array is stored as the SHA-256 of its canonical-order bytes
 (uint32 supports, int32 trussness, uint8 masks) plus its histogram, so a
 mismatch also shows where the counts differ.  O-3 vs O-4 is checked here
 (Σ support = 3 T, P4).  Phase times, thread counts and the CPU model are
 recorded: they are the full oracle runs the bench report quotes.
 
-    python scripts/make_golden.py C3 [C4 C5]    (C5: ~45 GB RAM, hours)
+    python scripts/make_golden.py [--tau o7|o8|both] C3 [C4 C5]    (C5: ~45 GB RAM, hours)
 
 Arrays are cached under exp/golden_cache/ (git- and gpurun-ignored) so a
 rerun resumes after the support pass.
@@ -66,7 +70,7 @@ def hist(a: np.ndarray) -> dict:
     return {str(int(x)): int(c) for x, c in zip(vals, cnt)}
 
 
-def run(name: str, ktruss_batch: tuple = ()) -> dict:
+def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
     os.makedirs(CACHE, exist_ok=True)
     cfg = gen.CONFIGS[name]
     times = {}
@@ -114,10 +118,20 @@ def run(name: str, ktruss_batch: tuple = ()) -> dict:
         out.setdefault("ktruss_rounds", {})[str(k)] = trace.tolist()
         log(name, f"O-5 k={k}: {int(alive.sum())} edges, {trace.size} rounds, {times[f'ktruss{k}_s']:.1f}s")
 
-    t = time.time()
-    tau, kmax = g.truss_sequential(sup, consume=True)      # O-7 (uses the rows in place)
-    times["truss_sequential_s"] = time.time() - t
-    log(name, "O-7 kmax", kmax, f"{times['truss_sequential_s']:.1f}s")
+    if tau_mode in ("o7", "both"):
+        t = time.time()
+        tau, kmax = g.truss_sequential(sup, consume=(tau_mode == "o7"))   # O-7 (rows in place when alone)
+        times["truss_sequential_s"] = time.time() - t
+        log(name, "O-7 kmax", kmax, f"{times['truss_sequential_s']:.1f}s")
+    if tau_mode in ("o8", "both"):
+        t = time.time()
+        tau8, kmax8 = g.truss_parallel(sup, consume=True)                  # O-8
+        times["truss_parallel_s"] = time.time() - t
+        log(name, "O-8 kmax", kmax8, f"{times['truss_parallel_s']:.1f}s")
+        if tau_mode == "both":
+            assert kmax8 == kmax and np.array_equal(tau8, tau), "O-7 and O-8 disagree"
+        tau, kmax = tau8, kmax8
+    out["trussness_oracle"] = {"o7": "O-7", "o8": "O-8", "both": "O-7 = O-8 (checked equal)"}[tau_mode]
     np.save(os.path.join(CACHE, f"{name}_tau.npy"), tau)
     for k, alive in masks.items():
         assert np.array_equal(alive.astype(bool), tau >= k), f"O-5 k={k} != O-7 tau >= k (reading A8)"
@@ -130,15 +144,19 @@ def run(name: str, ktruss_batch: tuple = ()) -> dict:
         out["ktruss_sha256"][str(k)] = sha(mk)
     out["oracle_times"] = {**{k: round(v, 3) for k, v in times.items()},
                            "threads": os.cpu_count(), "truss_sequential_threads": 1,
+                           "truss_parallel_threads": os.cpu_count(),
                            "cpu": cpu_model(), "host": platform.node()}
     return out
 
 
 def main(argv):
+    tau_mode = None
+    if argv and argv[0] == "--tau":
+        tau_mode, argv = argv[1], argv[2:]
     names = argv or ["C3"]
     for name in names:
         ks = (3, 4, 5, 6) if name == "C3" else ()
-        d = run(name, ks)
+        d = run(name, ks, tau_mode or ("o8" if name == "C5" else "o7"))
         path = os.path.join(GOLDEN, f"{name.lower()}_expected.json")
         with open(path, "w") as f:
             json.dump(d, f, indent=1, sort_keys=True)

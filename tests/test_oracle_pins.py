@@ -193,6 +193,8 @@ def test_golden_examples(fixture):
     assert tau.tolist() == d["trussness"] and kmax == d["kmax"]
     tau2, kmax2 = g.truss_sequential()
     assert tau2.tolist() == d["trussness"] and kmax2 == d["kmax"]
+    tau3, kmax3 = g.truss_parallel()
+    assert tau3.tolist() == d["trussness"] and kmax3 == d["kmax"]
 
 
 def test_k4_ear_needs_single_decrement():
@@ -219,6 +221,8 @@ def test_complete_graph_closed_form(n):
     assert np.all(tau == n) and kmax == n
     tau2, kmax2 = g.truss_sequential()
     assert np.all(tau2 == n) and kmax2 == n
+    tau3, kmax3 = g.truss_parallel()
+    assert np.all(tau3 == n) and kmax3 == n
 
 
 def _triangle_free_cases():
@@ -460,6 +464,8 @@ def test_truss_properties_and_tiers_agree():
         tau, kmax = g.truss_decomposition()
         tau2, kmax2 = g.truss_sequential()
         assert np.array_equal(tau, tau2) and kmax == kmax2
+        tau3, kmax3 = g.truss_parallel()
+        assert np.array_equal(tau, tau3) and kmax == kmax3
         prev = None
         for k in range(2, kmax + 2):
             alive, _ = g.ktruss(k)
@@ -527,6 +533,10 @@ def test_hypothesis_oracle(raw):
     tau, kmax = g.truss_decomposition()
     tau2, kmax2 = g.truss_sequential()
     assert np.array_equal(tau, tau2) and kmax == kmax2
+    tau3, kmax3 = g.truss_parallel()
+    assert np.array_equal(tau, tau3) and kmax == kmax3
+    tau3, kmax3 = g.truss_parallel()
+    assert np.array_equal(tau, tau3) and kmax == kmax3
     if g.m:
         G = nx_graph(g)
         idx = edge_index(g)
@@ -616,6 +626,8 @@ def test_hypothesis_hub_graphs(raw):
     tau, kmax = g.truss_decomposition()
     tau2, kmax2 = g.truss_sequential()
     assert np.array_equal(tau, tau2) and kmax == kmax2
+    tau3, kmax3 = g.truss_parallel()
+    assert np.array_equal(tau, tau3) and kmax == kmax3
 
 
 # ------------------------------------------ k-truss byte-model terms (§8(d)) --
@@ -683,3 +695,19 @@ def test_ktruss_work_terms_bruteforce():
             tot[0] += sm
             tot[1] += dc
         assert (wd["sum_min"], wd["decrements"]) == tuple(tot)
+
+
+def test_tier2_decompositions_larger_graphs():
+    """O-7 (sequential bucket peel) and O-8 (parallel incremental rounds) equal
+    O-6 (batch recompute, the definition) on R-MAT graphs with deep cores and a
+    skewed one, and O-8 does not depend on the thread count."""
+    for s, ef, seed, abc in [(12, 16, 5, (0.57, 0.19, 0.19)), (13, 8, 6, (0.65, 0.15, 0.15)),
+                             (11, 32, 7, (0.57, 0.19, 0.19))]:
+        u, v = gen.rmat(s, ef, *abc, seed=seed)
+        g = oracle.OracleGraph(u, v)
+        tau, kmax = g.truss_decomposition()
+        assert (g.truss_sequential()[0] == tau).all()
+        t8, k8 = g.truss_parallel()
+        assert np.array_equal(t8, tau) and k8 == kmax
+        g1 = oracle.OracleGraph(u, v, nthreads=1)
+        assert np.array_equal(g1.truss_parallel()[0], tau)
