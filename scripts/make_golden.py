@@ -84,8 +84,9 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
     del u, v
     times["canonicalize_adjacency_s"] = time.time() - t
     log(name, "graph n", g.n, "m", g.m, f"{times['canonicalize_adjacency_s']:.1f}s")
-    out = {"_source": ("written by scripts/make_golden.py from oracle/ only (O-1..O-5, O-7; "
-                       "SURVEY.md §8(c)); per-edge arrays in canonical edge order (SURVEY §8(b))"),
+    out = {"_source": ("written by scripts/make_golden.py from oracle/ only (O-1..O-5; trussness by the "
+                       "tier-2 oracle named in trussness_oracle; SURVEY.md §8(c)); per-edge arrays in "
+                       "canonical edge order (SURVEY §8(b))"),
            "config": name, "desc": cfg.desc, "nnz": nnz, "n": g.n, "m": g.m,
            "canonical_sha256": sha(np.stack([g.cu, g.cv], axis=1))}
 
@@ -134,7 +135,7 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
     out["trussness_oracle"] = {"o7": "O-7", "o8": "O-8", "both": "O-7 = O-8 (checked equal)"}[tau_mode]
     np.save(os.path.join(CACHE, f"{name}_tau.npy"), tau)
     for k, alive in masks.items():
-        assert np.array_equal(alive.astype(bool), tau >= k), f"O-5 k={k} != O-7 tau >= k (reading A8)"
+        assert np.array_equal(alive.astype(bool), tau >= k), f"O-5 k={k} != tier-2 tau >= k (reading A8)"
     out.update(kmax=kmax, trussness_sha256=sha(tau.astype(np.int32)), trussness_hist=hist(tau))
     out["ktruss_size"] = {}
     out["ktruss_sha256"] = {}
