@@ -22,6 +22,7 @@ mismatch also shows where the counts differ.  O-3 vs O-4 is checked here
 recorded: they are the full oracle runs the bench report quotes.
 
     python scripts/make_golden.py [--tau o7|o8|both] C3 [C4 C5]    (C5: ~45 GB RAM, hours)
+    python scripts/make_golden.py --crosscheck C4   (O-8 against an O-7 golden, from the cache)
 
 Arrays are cached under exp/golden_cache/ (git- and gpurun-ignored) so a
 rerun resumes after the support pass.
@@ -150,7 +151,38 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
     return out
 
 
+def crosscheck(name: str) -> None:
+    """Re-derive the trussness of an existing golden with the other tier-2
+    oracle (O-8) from the cached supports and compare: the file then records
+    "O-7 = O-8 (checked equal)"."""
+    path = os.path.join(GOLDEN, f"{name.lower()}_expected.json")
+    d = json.load(open(path))
+    tau7 = np.load(os.path.join(CACHE, f"{name}_tau.npy"))
+    assert sha(tau7.astype(np.int32)) == d["trussness_sha256"], "cached trussness is not the golden's"
+    u, v = gen.CONFIGS[name].generate()
+    g = oracle.OracleGraph(u, v)
+    del u, v
+    sup = np.load(os.path.join(CACHE, f"{name}_support.npy"))
+    assert sha(sup.astype(np.uint32)) == d["support_sha256"]
+    t = time.time()
+    tau8, kmax8 = g.truss_parallel(sup, consume=True)
+    dt = time.time() - t
+    log(name, "O-8 kmax", kmax8, f"{dt:.1f}s")
+    assert kmax8 == d["kmax"] and np.array_equal(tau8, tau7), "O-7 and O-8 disagree"
+    d["trussness_oracle"] = "O-7 = O-8 (checked equal)"
+    d["oracle_times"]["truss_parallel_s"] = round(dt, 3)
+    d["oracle_times"]["truss_parallel_threads"] = os.cpu_count()
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1, sort_keys=True)
+        f.write("\n")
+    log("cross-checked", path)
+
+
 def main(argv):
+    if argv and argv[0] == "--crosscheck":
+        for name in argv[1:]:
+            crosscheck(name)
+        return
     tau_mode = None
     if argv and argv[0] == "--tau":
         tau_mode, argv = argv[1], argv[2:]
