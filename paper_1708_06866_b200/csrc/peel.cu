@@ -718,7 +718,7 @@ __global__ void k_offset_list(int32_t* __restrict__ list, const int* __restrict_
 }
 
 __global__ void k_u64_to_u32(const unsigned long long* __restrict__ a, uint32_t* __restrict__ b) {
-    if (threadIdx.x == 0) *b = (uint32_t)*a;
+    if (threadIdx.x == 0) *b = *a > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)*a;
 }
 
 // received decrements (NCCL partitioned peel): apply those of this rank's
@@ -1235,19 +1235,19 @@ static int peel_rounds_nccl(gc_ctx* c, uint32_t thr, int32_t level, int nf, int6
                 GC_TRY(launch_peel(c, blocks, A, pol, i1 - i0));
             }
             // sizes of every rank's send list, then the lists
-            GC_LAUNCH(c, k_u64_to_u32, 1, 32, 0, out_n, share + me);
+            GC_LAUNCH(c, k_u64_to_u32, 1, 32, 0, out_n, share + me);   // saturates past 2^32 - 1
             GC_TRY(allgather_u32(c, share + me, share, 1));
             GC_TRY(read_small(c, h, share, (size_t)P * 4));
-            GC_TRY(read_small(c, h + 64, out_n, 8));
             GC_TRY(sync(c));
-            if (*reinterpret_cast<uint64_t*>(h + 64) > (uint64_t)cap)
-                return fail(c, GC_ERR_RANGE, "partitioned peel: decrement list overflow");
             int64_t counts[64], offs[64], tot = 0;
             for (int r = 0; r < P; ++r) {
                 counts[r] = (uint32_t)h[r];
                 offs[r] = tot;
                 tot += counts[r];
             }
+            // every rank sees every count, so all of them stop together (cannot happen: K bounds the lists)
+            for (int r = 0; r < P; ++r)
+                if (counts[r] > cap) return fail(c, GC_ERR_RANGE, "partitioned peel: decrement list overflow");
             if (tot > 0) {
                 GC_TRY(allgatherv_i32(c, c->dec_out.as<int32_t>(), c->dec_in.as<int32_t>(), counts, offs));
                 GC_LAUNCH(c, k_apply_decrements, grid_for(tot), kThreads, 0, c->dec_in.as<int32_t>(), tot, lo, hi,
