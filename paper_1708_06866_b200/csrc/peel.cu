@@ -316,10 +316,11 @@ struct PeelArgs {
 };
 
 // Destroy the live triangles of each frontier edge e = (a, b): walk the
-// shorter endpoint row and binary-search each live entry in the longer one
-// (rows sorted by rank; dead entries compacted away now and then).  Stop
-// once S(e) live triangles are found (S exact only for the single-rank
-// policy).  A warp takes G frontier edges at a time (G = 1 for small
+// shorter endpoint row -- from its end: the highest-ranked (highest-degree)
+// third vertices close most triangles -- and binary-search each live entry
+// in the longer one (rows sorted by rank; dead entries compacted away now
+// and then).  Stop once S(e) live triangles are found (S exact for the
+// edges a rank enumerates).  A warp takes G frontier edges at a time (G = 1 for small
 // frontiers, up to 32 for big ones): lanes whose shorter row has at most
 // kSerialRow entries walk it alone (uniform-degree graphs: every lane busy),
 // the other edges are walked by the whole warp one after another.  Measured
@@ -328,6 +329,10 @@ struct PeelArgs {
 constexpr int kSerialRow = 8;
 #ifndef GC_GRP_MINB
 #define GC_GRP_MINB 4    // ... of k_peel_grouped (48 KB of shared memory per block)
+#endif
+#ifndef GC_PEEL_REVERSE
+#define GC_PEEL_REVERSE 1   // walk the shorter row from its end, highest ranks first (C4 k = 4 / 6 peel 39.3 -> 28.4 / 96.4 -> 61.6 ms,
+                            // decomposition 1.59 -> 1.49 s; C5 decomposition 19.5 -> 18.7 s); 0: from its start
 #endif
 #ifndef GC_PEEL_GMAX
 #define GC_PEEL_GMAX 8   // frontier edges per warp at most (8: K13 kernel 226 -> 78 ms, C4 +0.7 %)
@@ -364,20 +369,29 @@ __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol,
                                               int64_t a1, int64_t b0, int64_t b1, int lane) {
     uint32_t found = 0;
     // two 32-entry chunks of the shorter row per step, their searches interleaved
+#if GC_PEEL_REVERSE
+    // from the row's end: high-rank (high-degree) third vertices close most
+    // triangles, so an edge with few live triangles stops sooner
+    for (int64_t top = a1; top > a0 && found < live; top -= 64) {
+        const int64_t i0 = top - 64 + lane, i1 = top - 32 + lane;
+        const bool in0 = i0 >= a0, in1 = i1 >= a0;
+#else
     for (int64_t base = a0; base < a1 && found < live; base += 64) {
         const int64_t i0 = base + lane, i1 = base + 32 + lane;
+        const bool in0 = i0 < a1, in1 = i1 < a1;
+#endif
         int f0 = -1, f1 = -1;
         int32_t w0 = INT32_MAX, w1 = INT32_MAX;
-        if (i0 < a1) {
+        if (in0) {
             f0 = __ldg(A.sym_eid + i0);
             w0 = __ldg(A.sym_col + i0);
         }
-        if (i1 < a1) {
+        if (in1) {
             f1 = __ldg(A.sym_eid + i1);
             w1 = __ldg(A.sym_col + i1);
         }
-        const bool want0 = i0 < a1 && f0 != e && A.alive[f0];
-        const bool want1 = i1 < a1 && f1 != e && A.alive[f1];
+        const bool want0 = in0 && f0 != e && A.alive[f0];
+        const bool want1 = in1 && f1 != e && A.alive[f1];
         bool tri0 = false, tri1 = false;
         int g0 = -1, g1 = -1;
         if (want0 || want1) {
@@ -456,6 +470,23 @@ __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
         const bool serial = live && G > 1 && a1 - a0 <= kSerialRow;
         if (serial) {                                   // this lane alone
             uint32_t found = 0;
+#if GC_PEEL_REVERSE
+            int64_t hi = b1;
+            for (int64_t i = a1 - 1; i >= a0 && found < live; --i) {
+                const int f = __ldg(A.sym_eid + i);
+                if (f == e || !A.alive[f]) continue;
+                const int32_t w = __ldg(A.sym_col + i);
+                const int64_t j = lower_bound_i32(A.sym_col, b0, hi, w);   // targets descend along the row
+                if (j < hi && __ldg(A.sym_col + j) == w) {
+                    const int g = __ldg(A.sym_eid + j);
+                    if (A.alive[g]) {
+                        ++found;
+                        destroy(pol, e, f, g);
+                    }
+                }
+                hi = j;
+            }
+#else
             int64_t lo = b0;
             for (int64_t i = a0; i < a1 && found < live; ++i) {
                 const int f = __ldg(A.sym_eid + i);
@@ -470,6 +501,7 @@ __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
                     }
                 }
             }
+#endif
         }
         unsigned coop = __ballot_sync(0xffffffffu, live && !serial);
         while (coop) {                                  // the whole warp, one edge at a time
