@@ -228,7 +228,7 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
 // warp one eighth).  probe.loc(w) returns a handle (>= 0) when w is in N+(v), else -1;
 // probe.credit(handle) adds the (v,w)-role credit.
 template <bool SUP, bool CLIP, class Probe>
-__device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int64_t cb,
+__device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, int ca, int cb,
                                                 const int32_t* __restrict__ in_pos,
                                                 const int32_t* __restrict__ in_src,
                                                 const int64_t* __restrict__ in_cost,
@@ -246,12 +246,13 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t ca, int6
             beg = p + 1;
             len = (int)(__ldg(dag_ptr + u + 1) - (int64_t)beg);
             if (CLIP) {
-                const int64_t w0 = __ldg(in_cost + i) + kOvh;
-                int64_t lo = ca - w0, hi = cb - w0;
+                // cost units relative to the task's first in-edge (a task spans < 2^31 units)
+                const int w0 = (int)(__ldg(in_cost + i) - cbase) + kOvh;
+                int lo = ca - w0, hi = cb - w0;
                 lo = lo < 0 ? 0 : (lo > len ? len : lo);
                 hi = hi < 0 ? 0 : (hi > len ? len : hi);
-                beg += (int)lo;
-                len = (int)(hi - lo);
+                beg += lo;
+                len = hi - lo;
             }
         }
         // Long suffixes (the bulk of the wedges): one at a time with the whole
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(256, GC_WARP_MINB) k_tc_warp(KArgs a) {
         }
         __syncwarp();
         SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
-        hits += stream_task<SUP, false>(i0, i1, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
+        hits += stream_task<SUP, false>(i0, i1, 0, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
                                         H, lane, a.long_seg, a.uw);
         if (SUP) {
             __syncwarp();
@@ -732,20 +733,21 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
         // this warp's eighth of the task's cost units
         const int64_t c0 = __ldg(a.in_cost + i0), c1 = __ldg(a.in_cost + i1);
         const int64_t ca = c0 + (c1 - c0) * warp / BW, cb = c0 + (c1 - c0) * (warp + 1) / BW;
+        const int ca32 = (int)(ca - c0), cb32 = (int)(cb - c0);
         if (cb > ca) {
             const int first = (int)warp_lower_bound(a.in_cost, i0, i1, ca + 1, lane) - 1;
             const int end = (int)warp_lower_bound(a.in_cost, i0, i1, cb, lane);
             if (use_gp) {
                 GlobalProbe G{a.dag_col + r0, d, r0};
-                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, G, lane, a.long_seg, a.uw);
             } else if (use_bm) {
                 SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u};
-                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, B, lane, a.long_seg, a.uw);
             } else {
                 SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
-                hits += stream_task<SUP, true>(first, end, ca, cb, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
+                hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
                                                a.dag_col, a.sup, H, lane, a.long_seg, a.uw);
             }
         }
