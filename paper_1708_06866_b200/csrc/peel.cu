@@ -334,6 +334,10 @@ constexpr int kSerialRow = 8;
 #define GC_PEEL_REVERSE 1   // walk the shorter row from its end, highest ranks first (C4 k = 4 / 6 peel 39.3 -> 28.4 / 96.4 -> 61.6 ms,
                             // decomposition 1.59 -> 1.49 s; C5 decomposition 19.5 -> 18.7 s); 0: from its start
 #endif
+#ifndef GC_PEEL_FIRST32
+#define GC_PEEL_FIRST32 1   // the walk's first step searches 32 entries, later ones 64 (C4 k = 4 / 6 peel -5 % / -6 %,
+                            // C4 decomposition +1 %, C5 decomposition -1 %); 0: 64 from the start
+#endif
 #ifndef GC_PEEL_GMAX
 #define GC_PEEL_GMAX 8   // frontier edges per warp at most (8: K13 kernel 226 -> 78 ms, C4 +0.7 %)
 #endif
@@ -372,9 +376,17 @@ __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol,
 #if GC_PEEL_REVERSE
     // from the row's end: high-rank (high-degree) third vertices close most
     // triangles, so an edge with few live triangles stops sooner
+#if GC_PEEL_FIRST32
+    // the first step takes only the top 32 entries: an edge with one or two
+    // live triangles usually finds them there
+    for (int64_t top = a1, step = 32; top > a0 && found < live; top -= step, step = 64) {
+        const int64_t i0 = top - 64 + lane, i1 = top - 32 + lane;
+        const bool in0 = step == 64 && i0 >= a0, in1 = i1 >= a0;
+#else
     for (int64_t top = a1; top > a0 && found < live; top -= 64) {
         const int64_t i0 = top - 64 + lane, i1 = top - 32 + lane;
         const bool in0 = i0 >= a0, in1 = i1 >= a0;
+#endif
 #else
     for (int64_t base = a0; base < a1 && found < live; base += 64) {
         const int64_t i0 = base + lane, i1 = base + 32 + lane;
