@@ -193,40 +193,58 @@ __host__ __device__ __forceinline__ uint8_t st_front(int32_t round) { return (ui
 // An edge below the threshold with S(e) = 0 lies in no live triangle, so it
 // is removed on the spot (nothing to destroy, nobody sees it in this round);
 // the others go to the frontier list for the peel kernel.
-__global__ void k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restrict__ alive,
+__global__ void __launch_bounds__(256) k_frontier_scan(const uint32_t* __restrict__ S, uint8_t* __restrict__ alive,
                                 const int32_t* __restrict__ list, int64_t len, uint32_t thr,
                                 int32_t round, int32_t* __restrict__ front,
                                 int* __restrict__ count, int32_t* __restrict__ tau, int32_t level,
                                 unsigned long long* __restrict__ zero_removed, uint32_t* __restrict__ min_rest,
                                 int32_t* __restrict__ zlist, int* __restrict__ zcount) {
-    const int lane = threadIdx.x & 31;
+    // the frontier is appended block-aggregated: one global atomic per block
+    // tile instead of one per warp (a big first frontier, e.g. every S = 1
+    // edge at k = 4, made the shared counter the scan's bottleneck)
+    __shared__ int woff[8];
+    __shared__ int bbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned zeros = 0;
     uint32_t rest = 0xFFFFFFFFu;   // min S over the alive edges left out of the frontier
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e = list ? (int64_t)list[i] : i;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t tile = (int64_t)blockIdx.x * blockDim.x; tile < len; tile += stride) {   // uniform per block
+        const int64_t i = tile + threadIdx.x;
+        int64_t e = -1;
         bool in = false;
-        if (alive[e]) {
-            const uint32_t se = S[e];
-            if (se == 0 && thr > 0) {
-                alive[e] = 0;
-                if (tau) tau[e] = level;
-                if (zlist) zlist[atomicAdd(zcount, 1)] = (int32_t)e;   // work stats only
-                ++zeros;
-            } else {
-                in = se < thr;
-                if (!in) rest = min(rest, se);
+        if (i < len) {
+            e = list ? (int64_t)list[i] : i;
+            if (alive[e]) {
+                const uint32_t se = S[e];
+                if (se == 0 && thr > 0) {
+                    alive[e] = 0;
+                    if (tau) tau[e] = level;
+                    if (zlist) zlist[atomicAdd(zcount, 1)] = (int32_t)e;   // work stats only
+                    ++zeros;
+                } else {
+                    in = se < thr;
+                    if (!in) rest = min(rest, se);
+                }
             }
         }
-        unsigned ballot = __ballot_sync(__activemask(), in);
+        const unsigned ballot = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) woff[warp] = __popc(ballot);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                const int c = woff[w];
+                woff[w] = tot;
+                tot += c;
+            }
+            bbase = tot ? atomicAdd(count, tot) : 0;
+        }
+        __syncthreads();
         if (in) {
             alive[e] = st_front(round);
-            // warp-aggregated append
-            int leader = __ffs(ballot) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(count, __popc(ballot));
-            base = __shfl_sync(ballot, base, leader);
-            front[base + __popc(ballot & ((1u << lane) - 1))] = (int32_t)e;
+            front[bbase + woff[warp] + __popc(ballot & ((1u << lane) - 1))] = (int32_t)e;
         }
+        __syncthreads();                     // woff / bbase are rewritten by the next tile
     }
     zeros = __reduce_add_sync(0xffffffffu, zeros);
     if (lane == 0 && zeros) atomicAdd(zero_removed, (unsigned long long)zeros);
@@ -258,7 +276,7 @@ struct PolicySingle {       // one rank: X = {st == st_front(round)}; crossings 
     __device__ __forceinline__ void dec(int f) const {
         if (atomicSub(S + f, 1u) == thr) {
             st[f] = st_front(round + 1);
-            next[atomicAdd(next_count, 1)] = f;
+            next[atomicAdd(next_count, 1)] = f;   // (warp-aggregating this append cost the decomposition 1 %)
         }
     }
 };
