@@ -244,7 +244,7 @@ int gc_destroy(gc_ctx* c) {
     gcx::Buf* bufs[] = {&c->raw_u, &c->raw_v, &c->stage_u, &c->stage_v, &c->canon, &c->deg, &c->rank_of, &c->dag_ptr,
                         &c->dag_col, &c->dag_src, &c->dag_eid, &c->in_ptr, &c->in_pos, &c->in_src,
                         &c->in_dst, &c->task_i0, &c->task_i1, &c->in_cost, &c->tmp_a, &c->tmp_b, &c->keys_a, &c->keys_b,
-                        &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
+                        &c->vals_a, &c->vals_b, &c->cub_tmp, &c->scal, &c->sup, &c->uw16, &c->out_tmp, &c->out_tmp2, &c->id_of, &c->list_out, &c->batch_slot, &c->grp_keys, &c->grp_vals, &c->grp_starts, &c->grp_flags, &c->grp_light,
                         &c->sym_ptr, &c->sym_col, &c->sym_eid, &c->alive, &c->front_a,
                         &c->front_b, &c->tau, &c->xbits, &c->nbits, &c->zbits, &c->sup_parts, &c->live_len, &c->long_rows, &c->alist,
                         &c->vdeg, &c->zlist, &c->task_pref, &c->dec_out, &c->dec_in};

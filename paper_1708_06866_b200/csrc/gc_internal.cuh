@@ -128,6 +128,7 @@ struct gc_ctx {
     gcx::Buf cub_tmp;
     gcx::Buf scal;              // small device scalars (counters, reductions)
     gcx::Buf sup;               // uint32[m] support in DAG-position order
+    gcx::Buf uw16;              // uint16[m] (u,w)-role credits of the support pass (folded into sup)
     gcx::Buf out_tmp;           // staging for canonical-order outputs
     gcx::Buf out_tmp2;          // second staging buffer (fused analysis: support and mask)
     gcx::Buf id_of;             // int32[n] rank -> original id (triangle listing)

@@ -42,6 +42,12 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 #ifndef GC_KOVH
 #define GC_KOVH 128
 #endif
+#ifndef GC_UW16
+#define GC_UW16 1          // (u,w) credits into a separate uint16[m] array (folded into the supports after the
+                           // pass): four adjacent positions per 64-bit atomic, half the L2 footprint of the
+                           // scattered role.  A count never exceeds d+(u) <= sqrt(2m) < 2^16 (m < 2^31), so
+                           // the 16-bit lanes never carry.  0: 32-bit credits straight into the supports
+#endif
 #ifndef GC_PAIR_CREDIT
 #define GC_PAIR_CREDIT 1   // (u,w) credits of adjacent positions paired into 64-bit atomics (C4 / C5 support
                            // pass 99.8 -> 95.3 / 1,282 -> 1,122 ms); 0: one 32-bit atomic per credit
@@ -222,6 +228,18 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
     if (threadIdx.x < 4 && bh[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)bh[threadIdx.x]);
 }
 
+// role (u,w) of one position q: into the uint16 array (the 32-bit word holding
+// it; the lanes never carry) or straight into the supports
+__device__ __forceinline__ void credit_uw(uint32_t* __restrict__ sup, uint16_t* __restrict__ uw16, int64_t q) {
+#if GC_UW16
+    (void)sup;
+    atomicAdd(reinterpret_cast<unsigned*>(uw16 + (q & ~(int64_t)1)), 1u << ((unsigned)(q & 1) << 4));
+#else
+    (void)uw16;
+    atomicAdd(sup + q, 1u);
+#endif
+}
+
 // ------------------------------------------------------- stream routine --
 // Walk the suffixes of the in-edges [i0, i1), 32 in-edges per group,
 // flattening their wedges across the 32 lanes so short and long suffixes
@@ -238,7 +256,8 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                                                 const int64_t* __restrict__ in_cost,
                                                 const int64_t* __restrict__ dag_ptr,
                                                 const int32_t* __restrict__ dag_col, uint32_t* __restrict__ sup,
-                                                Probe& probe, int lane, int long_seg, int uw) {
+                                                uint16_t* __restrict__ uw16, Probe& probe, int lane, int long_seg,
+                                                int uw) {
     uint32_t hits = 0;
     for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
@@ -277,7 +296,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                     if (inr && hd >= 0) {
                         ++seg_hits;
                         if (!(uw & 2)) probe.credit(hd, sup);     // role (v,w)
-                        if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
+                        if (!(uw & 1)) credit_uw(sup, uw16, q);   // role (u,w)
                     }
                 }
             };
@@ -314,19 +333,27 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                         if (k3) probe.credit(h3, sup);
                     }
                     if (!(uw & 1)) {
+#if GC_UW16
+                        // the four positions q0..q0+3 (q0 a multiple of 4): one 64-bit atomic
+                        if (k0 | k1 | k2 | k3)
+                            atomicAdd(reinterpret_cast<unsigned long long*>(uw16 + q0),
+                                      (unsigned long long)k0 | ((unsigned long long)k1 << 16) |
+                                          ((unsigned long long)k2 << 32) | ((unsigned long long)k3 << 48));
+#else
                         if (k0 | k1)
                             atomicAdd(reinterpret_cast<unsigned long long*>(sup + q0),
                                       ((unsigned long long)k1 << 32) | k0);
                         if (k2 | k3)
                             atomicAdd(reinterpret_cast<unsigned long long*>(sup + q0 + 2),
                                       ((unsigned long long)k3 << 32) | k2);
+#endif
                     }
 #else
                     auto take = [&](int q, int hd) {
                         if ((uint32_t)(q - b) < (uint32_t)(e - b) && hd >= 0) {
                             ++seg_hits;
                             if (!(uw & 2)) probe.credit(hd, sup);     // role (v,w)
-                            if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
+                            if (!(uw & 1)) credit_uw(sup, uw16, q);   // role (u,w)
                         }
                     };
                     take(q0, h0); take(q0 + 1, h1); take(q0 + 2, h2); take(q0 + 3, h3);
@@ -383,7 +410,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                         hit = true;
                         ++hits;
                         if (!(uw & 2)) probe.credit(slot, sup);   // role (v,w)
-                        if (!(uw & 1)) atomicAdd(sup + q, 1u);   // role (u,w)
+                        if (!(uw & 1)) credit_uw(sup, uw16, q);   // role (u,w)
                     }
                 }
             }
@@ -444,6 +471,7 @@ struct KArgs {
     const int64_t* task_pref;   // exclusive cost prefix over the tasks (this class's slice)
     int64_t cls_start, cls_total;   // ... the class's first prefix value and its total cost
     uint32_t* sup;
+    uint16_t* uw16;             // (u,w)-role credits (GC_UW16), folded into sup after the pass
     unsigned long long* count;
     uint32_t bm_bits;           // bitmap capacity of the heavy-head kernel (0: hash only)
     int long_seg;               // suffix length threshold of the warp-vector path
@@ -507,7 +535,7 @@ __global__ void __launch_bounds__(256, GC_TINY_MINB) k_tc_tiny(KArgs a) {
                 if (mk) {
                     ++seg;
                     if (SUP) {
-                        if (!(a.uw & 1)) atomicAdd(a.sup + q, 1u);                     // role (u,w)
+                        if (!(a.uw & 1)) credit_uw(a.sup, a.uw16, q);                  // role (u,w)
                         if (!(a.uw & 2)) atomicAdd(a.sup + r0 + (__ffs(mk) - 1), 1u);  // role (v,w)
                     }
                 }
@@ -555,7 +583,7 @@ __global__ void __launch_bounds__(256, GC_WARP_MINB) k_tc_warp(KArgs a) {
         __syncwarp();
         SmemHash<SUP> H{keys, vals, cnt, lg, (uint32_t)(ts - 1)};
         hits += stream_task<SUP, false>(i0, i1, 0, 0, 0, a.in_pos, a.in_src, a.in_cost, a.dag_ptr, a.dag_col, a.sup,
-                                        H, lane, a.long_seg, a.uw);
+                                        a.uw16, H, lane, a.long_seg, a.uw);
         if (SUP) {
             __syncwarp();
             for (int j = lane; j < ts; j += 32)
@@ -770,15 +798,15 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
             if (use_gp) {
                 GlobalProbe G{a.dag_col + r0, d, r0};
                 hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, G, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, a.uw16, G, lane, a.long_seg, a.uw);
             } else if (use_bm) {
                 SmemBitmap<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u};
                 hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, B, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, a.uw16, B, lane, a.long_seg, a.uw);
             } else {
                 SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)(ts - 1)};
                 hits += stream_task<SUP, true>(first, end, c0, ca32, cb32, a.in_pos, a.in_src, a.in_cost, a.dag_ptr,
-                                               a.dag_col, a.sup, H, lane, a.long_seg, a.uw);
+                                               a.dag_col, a.sup, a.uw16, H, lane, a.long_seg, a.uw);
             }
         }
     }
@@ -786,6 +814,24 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     }
     if (cur >= 0) teardown(false);
     add_count(a.count, hits, lane);
+}
+
+// sup[p] += uw16[p], four positions per thread
+__global__ void k_fold_uw(uint32_t* __restrict__ sup, const uint16_t* __restrict__ uw16, int64_t m) {
+    const int64_t nq = m / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nq; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < nq) {
+            uint4 s = reinterpret_cast<uint4*>(sup)[i];
+            const uint2 w = reinterpret_cast<const uint2*>(uw16)[i];
+            s.x += w.x & 0xFFFFu;
+            s.y += w.x >> 16;
+            s.z += w.y & 0xFFFFu;
+            s.w += w.y >> 16;
+            reinterpret_cast<uint4*>(sup)[i] = s;
+        } else {
+            for (int64_t p = 4 * nq; p < m; ++p) sup[p] += uw16[p];
+        }
+    }
 }
 
 template <class T>
@@ -922,7 +968,8 @@ int prepare_tasks(gc_ctx* c) {
 
 // Launch every class kernel for owner `owner` of `parts`.
 template <bool SUP>
-static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* count, uint32_t* sup) {
+static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* count, uint32_t* sup,
+                          uint16_t* uw16) {
     KArgs a{};
     a.in_pos = c->in_pos.as<int32_t>();
     a.in_src = c->in_src.as<int32_t>();
@@ -934,6 +981,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     a.parts = parts;
     a.owner = owner;
     a.sup = sup;
+    a.uw16 = uw16;
     a.count = count;
     a.bm_bits = bm_bits_of(c);
     a.long_seg = c->long_seg;
@@ -1025,7 +1073,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
 }
 
 template <bool SUP>
-static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
+static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup, uint16_t* uw16) {
     if (!c->tasks_ready) GC_TRY(prepare_tasks(c));
     const int parts = c->task_parts;
     if (c->total_cost == 0) return GC_OK;
@@ -1036,7 +1084,7 @@ static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
             if (!c->pev[r]) GC_CUDA(c, cudaEventCreate(&c->pev[r]));
         for (int r = 0; r < parts; ++r) {
             if (r < nt) GC_CUDA(c, cudaEventRecord(c->pev[r], c->stream));
-            GC_TRY(launch_classes<SUP>(c, r, parts, count, sup));
+            GC_TRY(launch_classes<SUP>(c, r, parts, count, sup, uw16));
         }
         if (nt > 0) {
             GC_CUDA(c, cudaEventRecord(c->pev[nt], c->stream));
@@ -1051,7 +1099,7 @@ static int run_all_parts(gc_ctx* c, unsigned long long* count, uint32_t* sup) {
             }
         }
     } else {
-        GC_TRY(launch_classes<SUP>(c, c->rank, parts, count, sup));
+        GC_TRY(launch_classes<SUP>(c, c->rank, parts, count, sup, uw16));
     }
     return GC_OK;
 }
@@ -1063,7 +1111,7 @@ int triangle_count(gc_ctx* c, uint64_t* out) {
     GC_TRY(record(c, 2));
     GC_CUDA(c, cudaMemsetAsync(count, 0, 8, c->stream));
     GC_TRY(record(c, 6));
-    GC_TRY(run_all_parts<false>(c, count, nullptr));
+    GC_TRY(run_all_parts<false>(c, count, nullptr, nullptr));
     GC_TRY(record(c, 7));
     if (c->nccl) GC_TRY(allreduce_u64(c, reinterpret_cast<uint64_t*>(count), 1));
     GC_TRY(record(c, 3));
@@ -1082,8 +1130,19 @@ int support_dag(gc_ctx* c) {
     unsigned long long* count = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 200);
     GC_CUDA(c, cudaMemsetAsync(c->sup.p, 0, (size_t)m * 4, c->stream));
     GC_CUDA(c, cudaMemsetAsync(count, 0, 8, c->stream));
+    uint16_t* uw16 = nullptr;
+    if (GC_UW16 && m > 0) {
+        // d+(x) <= sqrt(2m) (x's higher-ranked neighbours all have degree >= d+(x)), so with
+        // m < 2^31 every (u,w) count is below 2^16 and the 16-bit lanes never carry
+        if (c->stats.max_out_degree > 65535) return fail(c, GC_ERR_RANGE, "support pass: d+ above 65535");
+        const size_t bytes = (size_t)((m + 3) / 4) * 8;   // whole 64-bit words
+        GC_TRY(ensure(c, c->uw16, bytes));
+        GC_CUDA(c, cudaMemsetAsync(c->uw16.p, 0, bytes, c->stream));
+        uw16 = c->uw16.as<uint16_t>();
+    }
     GC_TRY(record(c, 6));
-    GC_TRY(run_all_parts<true>(c, count, c->sup.as<uint32_t>()));
+    GC_TRY(run_all_parts<true>(c, count, c->sup.as<uint32_t>(), uw16));
+    if (uw16) GC_LAUNCH(c, k_fold_uw, grid_for((m + 3) / 4), kThreads, 0, c->sup.as<uint32_t>(), uw16, m);
     GC_TRY(record(c, 7));
     if (c->nccl) GC_TRY(allreduce_u32(c, c->sup.as<uint32_t>(), (size_t)m));
     return GC_OK;
