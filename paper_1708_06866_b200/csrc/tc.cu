@@ -228,16 +228,22 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
     if (threadIdx.x < 4 && bh[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)bh[threadIdx.x]);
 }
 
-// role (u,w) of one position q: into the uint16 array (the 32-bit word holding
-// it; the lanes never carry) or straight into the supports
-__device__ __forceinline__ void credit_uw(uint32_t* __restrict__ sup, uint16_t* __restrict__ uw16, int64_t q) {
+// roles (u,w) and (u,v) of DAG position q (an edge u -> x): into the uint16
+// array (the 32-bit word holding it) or straight into the supports.  The two
+// roles count disjoint parts of N+(u) \ {x} -- third vertices below x, and
+// above x -- so their sum is below d+(u) <= sqrt(2m) < 2^16: no lane carries.
+__device__ __forceinline__ void credit_u(uint32_t* __restrict__ sup, uint16_t* __restrict__ uw16, int64_t q,
+                                         uint32_t k) {
 #if GC_UW16
     (void)sup;
-    atomicAdd(reinterpret_cast<unsigned*>(uw16 + (q & ~(int64_t)1)), 1u << ((unsigned)(q & 1) << 4));
+    atomicAdd(reinterpret_cast<unsigned*>(uw16 + (q & ~(int64_t)1)), k << ((unsigned)(q & 1) << 4));
 #else
     (void)uw16;
-    atomicAdd(sup + q, 1u);
+    atomicAdd(sup + q, k);
 #endif
+}
+__device__ __forceinline__ void credit_uw(uint32_t* __restrict__ sup, uint16_t* __restrict__ uw16, int64_t q) {
+    credit_u(sup, uw16, q, 1u);
 }
 
 // ------------------------------------------------------- stream routine --
@@ -375,7 +381,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
             if (SUP) {
                 const uint32_t tot_hits = __reduce_add_sync(0xffffffffu, seg_hits);
                 const int ps = __shfl_sync(0xffffffffu, p, s);
-                if (lane == 0 && tot_hits && !(uw & 4)) atomicAdd(sup + ps, tot_hits);   // role (u,v)
+                if (lane == 0 && tot_hits && !(uw & 4)) credit_u(sup, uw16, ps, tot_hits);   // role (u,v)
             }
         }
         if (len >= long_seg) len = 0;
@@ -419,7 +425,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
                 if (hit && !(uw & 4)) {
                     const unsigned grp = __match_any_sync(hm, s);
-                    if (lane == __ffs(grp) - 1) atomicAdd(sup + ps, (uint32_t)__popc(grp));
+                    if (lane == __ffs(grp) - 1) credit_u(sup, uw16, ps, (uint32_t)__popc(grp));
                 }
             }
         }
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(256, GC_TINY_MINB) k_tc_tiny(KArgs a) {
                 }
             }
             hits += seg;
-            if (SUP && seg && !(a.uw & 4)) atomicAdd(a.sup + p, seg);                   // role (u,v)
+            if (SUP && seg && !(a.uw & 4)) credit_u(a.sup, a.uw16, p, seg);             // role (u,v)
         }
     }
     add_count(a.count, hits, lane);
