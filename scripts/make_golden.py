@@ -24,6 +24,10 @@ recorded: they are the full oracle runs the bench report quotes.
     python scripts/make_golden.py [--tau o7|o8|both] C3 [C4 C5]    (C5: ~45 GB RAM, hours)
     python scripts/make_golden.py --crosscheck C4   (O-8 against an O-7 golden, from the cache)
     python scripts/make_golden.py --o4 C5           (O-4's triangle count against a golden's)
+    python scripts/make_golden.py --support-only C5 (T and supports only: trussness_pending)
+
+GOLDEN_CACHE=<dir> overrides the cache directory (e.g. supports computed on
+one host, the trussness on another).
 
 Arrays are cached under exp/golden_cache/ (git- and gpurun-ignored) so a
 rerun resumes after the support pass.
@@ -45,7 +49,7 @@ sys.path.insert(0, ROOT)
 import gen      # noqa: E402
 import oracle   # noqa: E402
 
-CACHE = os.path.join(ROOT, "exp", "golden_cache")
+CACHE = os.environ.get("GOLDEN_CACHE") or os.path.join(ROOT, "exp", "golden_cache")
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
@@ -72,7 +76,7 @@ def hist(a: np.ndarray) -> dict:
     return {str(int(x)): int(c) for x, c in zip(vals, cnt)}
 
 
-def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
+def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only: bool = False) -> dict:
     os.makedirs(CACHE, exist_ok=True)
     cfg = gen.CONFIGS[name]
     times = {}
@@ -120,6 +124,12 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7") -> dict:
     out.update(triangles=T, support_sha256=sha(sup.astype(np.uint32)), support_max=int(sup.max(initial=0)),
                support_zero=int((sup == 0).sum()))
 
+    if support_only:
+        # T and supports only (O-3, P4); the trussness is added by a later full run
+        out["trussness_pending"] = True
+        out["oracle_times"] = {**{k: round(v, 3) for k, v in times.items()}, "threads": os.cpu_count(),
+                               "cpu": cpu_model(), "host": platform.node()}
+        return out
     masks = {}
     for k in ktruss_batch:                                  # O-5, the definition
         t = time.time()
@@ -216,12 +226,15 @@ def main(argv):
             crosscheck(name)
         return
     tau_mode = None
+    support_only = False
+    if argv and argv[0] == "--support-only":
+        support_only, argv = True, argv[1:]
     if argv and argv[0] == "--tau":
         tau_mode, argv = argv[1], argv[2:]
     names = argv or ["C3"]
     for name in names:
         ks = (3, 4, 5, 6) if name == "C3" else ()
-        d = run(name, ks, tau_mode or ("o8" if name == "C5" else "o7"))
+        d = run(name, ks, tau_mode or ("o8" if name == "C5" else "o7"), support_only)
         path = os.path.join(GOLDEN, f"{name.lower()}_expected.json")
         with open(path, "w") as f:
             json.dump(d, f, indent=1, sort_keys=True)
