@@ -289,7 +289,8 @@ typedef struct gc_stats {
     int64_t q_in;             /* sum d-(x) d+(x) */
     int64_t max_out_degree;   /* max d+ */
     int64_t max_degree;       /* max d */
-    int64_t tasks[4];         /* intersection tasks per kernel class (last build) */
+    int64_t tasks[5];         /* intersection tasks per kernel class (last build): 0 lane, 1 warp,
+                                 2 block (bitmap or hash), 3 huge (hash), 4 wide bitmap */
     int64_t aux[8];           /* heads with d+ > 256 by rank span of N+ (<=2^17, 2^18,
                                  2^19, more): counts [0..3], in-degree weighted [4..7] */
     int64_t peel_sum_min;     /* GC_OPT_WORK_STATS, last peel: sum over rounds, over frontier

@@ -15,6 +15,8 @@
 
 namespace gcx {
 
+constexpr int kClasses = 5;   // intersection kernel classes: 0 lane, 1 warp, 2 block, 3 huge, 4 wide bitmap
+
 struct Buf {
     void* p = nullptr;
     size_t cap = 0;
@@ -62,7 +64,7 @@ struct gc_ctx {
     cudaStream_t side = nullptr;     // library-owned side stream (warp-task classes overlap the block kernels)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int overlap = 1;                 // GC_OPT_OVERLAP
-    int launch_grid[4][2] = {};      // intersection kernels: occupancy grid per class and SUP (0: not yet set up)
+    int launch_grid[5][2] = {};      // intersection kernels: occupancy grid per class and SUP (0: not yet set up)
     std::string err;
     bool poisoned = false;
     int state = 0;  // 0 created, 1 edges loaded, 2 graph built
@@ -114,11 +116,11 @@ struct gc_ctx {
     gcx::Buf task_i1;   // int32 one past the last in-list index of each task
     gcx::Buf in_cost;   // int64[m] exclusive cost prefix over the in-list
     gcx::Buf tmp_a, tmp_b;  // task construction scratch
-    int64_t ntask[4] = {0, 0, 0, 0};
-    int64_t task_off[5] = {0, 0, 0, 0, 0};
+    int64_t ntask[5] = {0, 0, 0, 0, 0};      // per intersection class (gcx::kClasses)
+    int64_t task_off[6] = {0, 0, 0, 0, 0, 0};
     int64_t total_cost = 0;
     gcx::Buf task_pref;     // int64 exclusive cost prefix over the class-sorted tasks (multi-owner cut)
-    int64_t cls_start[4] = {0, 0, 0, 0}, cls_total[4] = {1, 1, 1, 1};
+    int64_t cls_start[5] = {0, 0, 0, 0, 0}, cls_total[5] = {1, 1, 1, 1, 1};
     int task_parts = 1;     // number of owners the tasks were cut for
     bool tasks_ready = false;
 

@@ -57,6 +57,7 @@ constexpr int kOvh = GC_KOVH;               // per in-edge overhead in the cost 
 #define GC_KD1 128
 #endif
 constexpr int kD0 = 8, kD1 = GC_KD1, kD2 = 4096;    // class bounds on d+(v)
+constexpr int kD4 = 8192;                           // class 4 (wide bitmap): d+ bound
 constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
 constexpr int kTS1 = pow2_at_least(2 * kD1);   // class-1 warp hash slots: load <= 1/2 at d+ = kD1
 static_assert((kTS1 & (kTS1 - 1)) == 0 && kTS1 >= 2 * kD1, "class-1 table: power of two, load <= 1/2");
@@ -107,6 +108,9 @@ constexpr int kWarps = 8;                   // 256 threads per block
 #ifndef GC_TC_MINB
 #define GC_TC_MINB 5
 #endif
+#ifndef GC_WIDE_MINB
+#define GC_WIDE_MINB 3                      // class-4 support kernel (72 KB of shared memory: 3 blocks per SM)
+#endif
 
 // Kernel class of head v: 0/1 warp tasks (hash of N+(v) per warp), 2 block
 // tasks (rank-window bitmap if N+(v) spans <= bm_bits ranks, else hash when
@@ -126,6 +130,10 @@ __device__ __forceinline__ int head_class(const int64_t* __restrict__ dag_ptr, c
     if (c == 2) {
         const uint32_t span = d > 0 ? (uint32_t)dag_col[r0 + d - 1] - (uint32_t)v : 0u;
         if (d > kD2 || (span > bm_bits && d > kD2H)) c = 3;
+        // class 4: too many (v,w) counters for the block kernel's 4096, but the
+        // rank window still holds N+(v): the bitmap kernel with 8192 counters
+        // (C5: every head of class 3 -- 7,614 heads, 22 % of the wedges)
+        if (c == 3 && force != 3 && d <= kD4 && span <= bm_bits) c = 4;
     }
     return c;
 }
@@ -160,7 +168,7 @@ __global__ void k_head_chunk(const int64_t* __restrict__ pref, const int64_t* __
         int64_t ch = 0;
         if (dag_ptr[v + 1] > dag_ptr[v] && pref[in_ptr[v + 1]] > pref[in_ptr[v]]) {
             const int cl = head_class(dag_ptr, dag_col, in_ptr, (int)v, force, bm_bits);
-            ch = cl >= 2 ? chunk * kWarps : cl == 0 ? min(chunk, kTinyChunk) : chunk;
+            ch = cl >= 2 ? chunk * kWarps : cl == 0 ? min(chunk, kTinyChunk) : chunk;   // 2, 3, 4: block tasks
         }
         hch[v] = ch;
     }
@@ -210,8 +218,8 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
                             const int64_t* __restrict__ dag_ptr, const int32_t* __restrict__ dag_col, int force,
                             uint32_t bm_bits, uint32_t* __restrict__ cls, uint64_t* __restrict__ packed,
                             unsigned long long* __restrict__ hist) {
-    __shared__ unsigned int bh[4];                 // per-block class histogram (one global atomic per class)
-    if (threadIdx.x < 4) bh[threadIdx.x] = 0;
+    __shared__ unsigned int bh[kClasses];          // per-block class histogram (one global atomic per class)
+    if (threadIdx.x < kClasses) bh[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ntask; j += (int64_t)gridDim.x * blockDim.x) {
         int i0 = sel[j];
@@ -225,7 +233,7 @@ __global__ void k_task_fill(const int32_t* __restrict__ sel, int64_t ntask, int6
         if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(bh + k, (unsigned)__popc(grp));
     }
     __syncthreads();
-    if (threadIdx.x < 4 && bh[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)bh[threadIdx.x]);
+    if (threadIdx.x < kClasses && bh[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)bh[threadIdx.x]);
 }
 
 // roles (u,w) and (u,v) of DAG position q (an edge u -> x): into the uint16
@@ -677,15 +685,16 @@ struct GlobalProbe {
     __device__ __forceinline__ uint32_t hit(uint32_t w) const { return find(w) >= 0; }
 };
 
-template <bool SUP, bool HUGE>
+template <bool SUP, bool HUGE, int KD = kD2>   // KD: bitmap-mode (v,w) counters (kD4 for class 4)
 __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS),
-                                  HUGE ? (SUP ? 1 : GC_HUGE_MINB_TC) : (SUP ? GC_SUP_MINB : GC_TC_MINB))
+                                  HUGE ? (SUP ? 1 : GC_HUGE_MINB_TC)
+                                       : (SUP ? (KD > kD2 ? GC_WIDE_MINB : GC_SUP_MINB) : GC_TC_MINB))
     k_tc_block(KArgs a) {
     constexpr int BW = HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP_WARPS : GC_TC_WARPS;   // warps per block (= blockDim.x / 32)
     uint32_t* const smem = g_dsmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // layout (32-bit words): [0, kBW) bitmap | hash keys+vals ;
-    // SUP: [kBW, kBW + kBW/4) u16 prefix per 64-bit chunk | hash cnt ; then kD2 bitmap-mode cnt
+    // SUP: [kBW, kBW + kBW/4) u16 prefix per 64-bit chunk | hash cnt ; then KD bitmap-mode cnt
     // HUGE (class 3): [0, kTS3) keys | [kTS3, 2 kTS3) vals | [2 kTS3, 3 kTS3) cnt (SUP only)
     constexpr int kTSH = HUGE ? kTS3 : kTS2;
     constexpr int kZero = HUGE ? kTS3 : kBWS;    // words kept zero between heads
@@ -694,7 +703,7 @@ __global__ void __launch_bounds__(32 * (HUGE ? GC_HUGE_WARPS(SUP) : SUP ? GC_SUP
     int32_t* vals = reinterpret_cast<int32_t*>(smem + kTSH);
     uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);    // kBW/2 u16 = kBW/4 words
     uint32_t* hcnt = HUGE ? smem + 2 * kTS3 : smem + kBWS;        // hash mode: kTSH words
-    uint32_t* bcnt = smem + kBWS + kBW / 4;                        // bitmap mode: kD2 words
+    uint32_t* bcnt = smem + kBWS + kBW / 4;                        // bitmap mode: KD words
     static_assert(kTS2 <= kBW / 4 + kD2, "hash counters fit the SUP region");
     constexpr int max_lg = __builtin_ctz(kTSH);
     static_assert(2 * kTS2 <= kBW && kTS2 <= kBW / 2, "hash fits the bitmap region");
@@ -868,8 +877,8 @@ static uint32_t bm_bits_of(const gc_ctx* c) { return c->block_bitmap ? (uint32_t
 int prepare_tasks(gc_ctx* c) {
     const int64_t m = c->m;
     c->tasks_ready = false;
-    for (int k = 0; k < 4; ++k) c->ntask[k] = 0;
-    for (int k = 0; k < 5; ++k) c->task_off[k] = 0;
+    for (int k = 0; k < kClasses; ++k) c->ntask[k] = 0;
+    for (int k = 0; k <= kClasses; ++k) c->task_off[k] = 0;
     c->total_cost = 0;
     c->task_parts = c->loop_parts > 0 ? c->loop_parts : c->nranks;
     if (m == 0) {
@@ -922,8 +931,8 @@ int prepare_tasks(gc_ctx* c) {
     GC_TRY(read_small(c, h, d_nsel, 8));
     GC_TRY(sync(c));
     const int64_t nt = h[0];
-    unsigned long long* hist = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 160);
-    GC_CUDA(c, cudaMemsetAsync(hist, 0, 4 * 8, c->stream));
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 400);   // kClasses
+    GC_CUDA(c, cudaMemsetAsync(hist, 0, kClasses * 8, c->stream));
     uint32_t* cls = reinterpret_cast<uint32_t*>(c->keys_a.p);
     uint32_t* cls_sorted = cls + (m + 1);
     GC_LAUNCH(c, k_task_fill, grid_for(nt), kThreads, 0, sel, nt, m, c->in_dst.as<int32_t>(), c->in_ptr.as<int64_t>(),
@@ -931,22 +940,22 @@ int prepare_tasks(gc_ctx* c) {
               c->tmp_b.as<uint64_t>(), hist);
     tmp = 0;
     GC_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
-                                               c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
+                                               c->task_i0.as<uint64_t>(), nt, 0, 3, c->stream));
     GC_TRY(ensure(c, c->cub_tmp, tmp));
     tmp = c->cub_tmp.cap;
     GC_CUDA(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, cls, cls_sorted, c->tmp_b.as<uint64_t>(),
-                                               c->task_i0.as<uint64_t>(), nt, 0, 2, c->stream));
+                                               c->task_i0.as<uint64_t>(), nt, 0, 3, c->stream));
     c->stats.lib_launches += 3;
-    GC_TRY(read_small(c, h, hist, 4 * 8));
+    GC_TRY(read_small(c, h, hist, kClasses * 8));
     GC_TRY(sync(c));
     int64_t off = 0;
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kClasses; ++k) {
         c->ntask[k] = h[k];
         c->stats.tasks[k] = h[k];
         c->task_off[k] = off;
         off += h[k];
     }
-    c->task_off[4] = off;
+    c->task_off[kClasses] = off;
     if (c->task_parts > 1 && nt > 0) {
         // per-class 1D cut: exclusive cost prefix over the class-sorted tasks
         GC_TRY(ensure(c, c->task_pref, (size_t)(nt + 1) * 8));
@@ -960,10 +969,10 @@ int prepare_tasks(gc_ctx* c) {
         GC_CUDA(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp3, tcost, c->task_pref.as<int64_t>(), nt + 1,
                                                  c->stream));
         c->stats.lib_launches += 2;
-        for (int k = 0; k <= 4; ++k)
+        for (int k = 0; k <= kClasses; ++k)
             GC_TRY(read_small(c, h + 8 + k, c->task_pref.as<int64_t>() + c->task_off[k], 8));
         GC_TRY(sync(c));
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kClasses; ++k) {
             c->cls_start[k] = h[8 + k];
             c->cls_total[k] = std::max<int64_t>(1, h[9 + k] - h[8 + k]);
         }
@@ -998,7 +1007,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     // The warp-task classes (1, 0) run on a side stream forked from the
     // context stream, so they fill the SMs the block-task kernels (3, 2)
     // leave idle at their tails; the context stream joins it before return.
-    const bool fork = c->overlap && c->side && (c->ntask[3] > 0 || c->ntask[2] > 0) &&
+    const bool fork = c->overlap && c->side && (c->ntask[3] > 0 || c->ntask[2] > 0 || c->ntask[4] > 0) &&
                       (c->ntask[1] > 0 || c->ntask[0] > 0);
     cudaStream_t ws = fork ? c->side : c->stream;
     if (fork) {
@@ -1020,8 +1029,10 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
     // classes 3 and 2 first (heaviest tasks), then 1, 0
     unsigned long long* next = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 640);   // classes 3, 2
     if (GC_DYN_BATCH) GC_CUDA(c, cudaMemsetAsync(next, 0, 16, c->stream));
-    GC_TRY(ensure(c, c->batch_slot, 2 * 2 * 4096 * sizeof(long long)));   // classes 3 and 2, grid <= 4096
+    GC_TRY(ensure(c, c->batch_slot, 3 * 2 * 4096 * sizeof(long long)));   // classes 3, 2, 4; grid <= 4096
     long long* slots = c->batch_slot.as<long long>();
+    unsigned long long* next4 = reinterpret_cast<unsigned long long*>(c->scal.as<char>() + 448);   // class 4
+    if (GC_DYN_BATCH) GC_CUDA(c, cudaMemsetAsync(next4, 0, 8, c->stream));
     if (c->ntask[3] > 0) {
         a.next = GC_DYN_BATCH ? next : nullptr;
         a.slot = slots;
@@ -1035,6 +1046,30 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
         const int grid = prep(3, k_tc_block<SUP, true>, smem, threads);
         if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block huge)", __FILE__, __LINE__);
         GC_LAUNCH(c, (k_tc_block<SUP, true>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
+    }
+    if (c->ntask[4] > 0) {
+        // class 4: the bitmap kernel with 8192 (v,w) counters (support); the count
+        // pass needs no counters and runs these heads in the class-2 count kernel
+        a.next = GC_DYN_BATCH ? next4 : nullptr;
+        a.slot = slots + 2 * 2 * 4096;
+        a.tasks = tasks + c->task_off[4];
+        a.ntask = c->ntask[4];
+        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[4] : nullptr;
+        a.cls_start = c->cls_start[4];
+        a.cls_total = c->cls_total[4];
+        if (SUP) {
+            const size_t smem = (size_t)(kBWS + kBW / 4 + kD4) * sizeof(uint32_t);
+            constexpr int threads = 32 * GC_SUP_WARPS;
+            const int grid = prep(4, k_tc_block<SUP, false, kD4>, smem, threads);
+            if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block wide)", __FILE__, __LINE__);
+            GC_LAUNCH(c, (k_tc_block<SUP, false, kD4>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
+        } else {
+            const size_t smem = (size_t)kBWS * sizeof(uint32_t);
+            constexpr int threads = 32 * GC_TC_WARPS;
+            const int grid = prep(2, k_tc_block<SUP, false>, smem, threads);
+            if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_block)", __FILE__, __LINE__);
+            GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
+        }
     }
     if (c->ntask[2] > 0) {
         a.next = GC_DYN_BATCH ? next + 1 : nullptr;

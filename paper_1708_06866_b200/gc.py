@@ -67,7 +67,7 @@ class gc_stats(ctypes.Structure):
         ("compactions", ctypes.c_int64),
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("wedges", ctypes.c_int64),
         ("q_out", ctypes.c_int64), ("q_in", ctypes.c_int64), ("max_out_degree", ctypes.c_int64),
-        ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 4),
+        ("max_degree", ctypes.c_int64), ("tasks", ctypes.c_int64 * 5),
         ("aux", ctypes.c_int64 * 8),
         ("peel_sum_min", ctypes.c_int64), ("peel_decrements", ctypes.c_int64),
         ("part_ms", ctypes.c_double * 16), ("part_build_ms", ctypes.c_double * 16),

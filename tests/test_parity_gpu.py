@@ -437,8 +437,33 @@ def test_task_chunk_sizes(ctx, gcmod):
         ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 32768)
 
 
+def test_wide_bitmap_class(ctx, gcmod):
+    """Class 4 (4096 < d+ <= 8192, N+(v) inside the rank window: the bitmap
+    kernel with 8192 (v,w) counters) on a dense G(5000, 0.85): supports
+    against dense A^2 on the edges (P5), T = trace(A^3)/6, default and small
+    task chunks (a head split over several block tasks)."""
+    rng = np.random.default_rng(41)
+    n = 5000
+    u, v = random_graph(n, 0.85, rng)
+    A = np.zeros((n, n))
+    A[u, v] = 1
+    A[v, u] = 1
+    A2 = A @ A                                   # exact in float64 (entries < 2^53)
+    try:
+        for chunk in (32768, 2000):
+            ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, chunk)
+            run_gpu(ctx, u, v)
+            assert ctx.stats()["tasks"][4] > 0
+            cu, cv = ctx.get_edges()
+            sup = ctx.edge_support()
+            assert np.array_equal(sup, A2[cu, cv].astype(np.uint32))
+            assert ctx.triangle_count() == int(round(np.trace(A2 @ A))) // 6
+    finally:
+        ctx.set_option(gcmod.GC_OPT_TASK_CHUNK, 32768)
+
+
 def test_large_clique_all_classes(ctx):
-    """K_4200: out-degrees span every class including the > 4096 huge-head one."""
+    """K_4200: out-degrees span the classes up to the wide-bitmap one (4)."""
     n = 4200
     iu, ju = np.triu_indices(n, 1)
     run_gpu(ctx, iu.astype(np.int32), ju.astype(np.int32))
