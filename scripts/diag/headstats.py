@@ -42,3 +42,12 @@ sp = span[sel].float()
 for lo, hi in [(0, 2**17), (2**17, 2**18), (2**18, 2**20), (2**20, 2**30)]:
     m_ = (sp >= lo) & (sp < hi)
     print(f"span in [{lo},{hi}): heads {int(m_.sum())}, work {float(Ws[m_].sum()):.3e}")
+# class-3 composition (d+ > 4096, or span > 2^18 with d+ > 2048)
+c3 = (W > 0) & ((dplus > 4096) | ((span > 2**18) & (dplus > 2048)))
+print("class-3 heads", int(c3.sum()), "work", int(W[c3].sum()))
+for name, msk in [("2048<d<=4096, span>2^18", (dplus > 2048) & (dplus <= 4096) & (span > 2**18)),
+                  ("4096<d<=8192, span<=2^18", (dplus > 4096) & (dplus <= 8192) & (span <= 2**18)),
+                  ("4096<d<=8192, span>2^18", (dplus > 4096) & (dplus <= 8192) & (span > 2**18)),
+                  ("d>8192", dplus > 8192)]:
+    mm = c3 & msk
+    print(f"  {name}: heads {int(mm.sum())}, work {float(W[mm].sum()):.3e}, in-edges {int(din[mm].sum())}")
