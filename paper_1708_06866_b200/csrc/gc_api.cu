@@ -6,6 +6,14 @@
 #include <utility>
 
 #include "gc_internal.cuh"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range around every compute entry point (header-only NVTX v3: a no-op
+// unless a profiler injects itself; ncu --nvtx / nsys show the API calls)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace gcx {
 
@@ -327,6 +335,7 @@ static int drain_stage(gc_ctx* c) {
 }
 
 int gc_stage_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
+    NvtxRange nvtx_range("gc_stage_edges");
     GC_TRY(check_ctx(c));
     if (nnz < 0 || (nnz > 0 && (!u || !v))) return fail(c, GC_ERR_INVALID, "gc_stage_edges: bad arguments");
     cudaSetDevice(c->device);
@@ -351,6 +360,7 @@ int gc_stage_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
 }
 
 int gc_load_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
+    NvtxRange nvtx_range("gc_load_edges");
     GC_TRY(check_ctx(c));
     if (nnz < 0 || (nnz > 0 && (!u || !v))) return fail(c, GC_ERR_INVALID, "gc_load_edges: bad arguments");
     cudaSetDevice(c->device);
@@ -370,6 +380,7 @@ int gc_load_edges(gc_ctx* c, const int32_t* u, const int32_t* v, int64_t nnz) {
 }
 
 int gc_build_csr(gc_ctx* c) {
+    NvtxRange nvtx_range("gc_build_csr");
     GC_TRY(check_ctx(c));
     if (c->state < 1) return fail(c, GC_ERR_STATE, "gc_build_csr before gc_load_edges");
     cudaSetDevice(c->device);
@@ -413,6 +424,7 @@ int gc_num_edges(const gc_ctx* c, int64_t* m) {
 }
 
 int gc_triangle_count(gc_ctx* c, uint64_t* count) {
+    NvtxRange nvtx_range("gc_triangle_count");
     GC_TRY(check_ctx(c));
     if (!count) return fail(c, GC_ERR_INVALID, "gc_triangle_count: NULL output");
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_triangle_count before gc_build_csr");
@@ -421,6 +433,7 @@ int gc_triangle_count(gc_ctx* c, uint64_t* count) {
 }
 
 int gc_edge_support(gc_ctx* c, uint32_t* support_out) {
+    NvtxRange nvtx_range("gc_edge_support");
     GC_TRY(check_ctx(c));
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_edge_support before gc_build_csr");
     if (!support_out && c->m > 0) return fail(c, GC_ERR_INVALID, "gc_edge_support: NULL output");
@@ -439,6 +452,7 @@ int gc_edge_support(gc_ctx* c, uint32_t* support_out) {
 }
 
 int gc_ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
+    NvtxRange nvtx_range("gc_ktruss");
     GC_TRY(check_ctx(c));
     if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss: k must be >= 2 (P:280)");
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss before gc_build_csr");
@@ -450,6 +464,7 @@ int gc_ktruss(gc_ctx* c, int32_t k, uint8_t* alive_out, int64_t* m_alive) {
 
 int gc_ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
                        int64_t* m_alive) {
+    NvtxRange nvtx_range("gc_ktruss_analysis");
     GC_TRY(check_ctx(c));
     if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss_analysis: k must be >= 2 (P:280)");
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss_analysis before gc_build_csr");
@@ -460,6 +475,7 @@ int gc_ktruss_analysis(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* supp
 
 int gc_ktruss_analysis_async(gc_ctx* c, int32_t k, uint64_t* triangles, uint32_t* support_out, uint8_t* alive_out,
                              int64_t* m_alive) {
+    NvtxRange nvtx_range("gc_ktruss_analysis_async");
     GC_TRY(check_ctx(c));
     if (k < 2) return fail(c, GC_ERR_INVALID, "gc_ktruss_analysis_async: k must be >= 2 (P:280)");
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_ktruss_analysis_async before gc_build_csr");
@@ -481,6 +497,7 @@ int gc_wait(gc_ctx* c) {
 }
 
 int gc_truss_decomposition(gc_ctx* c, int32_t* tau_out, int32_t* kmax) {
+    NvtxRange nvtx_range("gc_truss_decomposition");
     GC_TRY(check_ctx(c));
     if (c->state < 2) return fail(c, GC_ERR_STATE, "gc_truss_decomposition before gc_build_csr");
     if (!kmax || (!tau_out && c->m > 0)) return fail(c, GC_ERR_INVALID, "gc_truss_decomposition: NULL output");
