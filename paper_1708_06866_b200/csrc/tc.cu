@@ -955,14 +955,30 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 2) k_tc_pipe(KArgs a) {
                     const bool use_bm = span <= a.bm_bits;
                     int lg = 0;
                     if (use_bm) {
-                        for (int j = lane; j < d; j += 32) {
-                            if (SUP) bcnt[j] = 0u;
-                            const uint32_t x = (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u;
-                            atomicOr(bits + (x >> 5), 1u << (x & 31));
-                            if (SUP) {
-                                const bool first = j == 0 ||
-                                    (((uint32_t)__ldg(a.dag_col + r0 + j - 1) - (uint32_t)v - 1u) >> 6) != (x >> 6);
-                                if (first) pre[x >> 6] = (uint16_t)j;
+                        // four rows' loads in flight per lane, then the inserts; the previous
+                        // entry of lane 0's element comes from lane 31 of the step before
+                        uint32_t carry = 0xFFFFFFFFu;   // window offset of entry j0 - 1 (none before 0)
+                        for (int j0 = 0; j0 < d; j0 += 128) {
+                            uint32_t x[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int j = j0 + 32 * k + lane;
+                                x[k] = j < d ? (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u : 0xFFFFFFFFu;
+                            }
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int j = j0 + 32 * k + lane;
+                                uint32_t prev = __shfl_up_sync(0xffffffffu, x[k], 1);
+                                const uint32_t last = __shfl_sync(0xffffffffu, x[k], 31);
+                                if (lane == 0) prev = carry;
+                                carry = last;
+                                if (j < d) {
+                                    atomicOr(bits + (x[k] >> 5), 1u << (x[k] & 31));
+                                    if (SUP) {
+                                        bcnt[j] = 0u;
+                                        if (j == 0 || (prev >> 6) != (x[k] >> 6)) pre[x[k] >> 6] = (uint16_t)j;
+                                    }
+                                }
                             }
                         }
                     } else {
