@@ -938,8 +938,13 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 2) k_tc_pipe(KArgs a) {
                     own &= ~mine;
                     // wait for the slot, then build segment seg's table in it
                     const int sl = seg & 1;
-                    if (lane == 0)
-                        while (*(volatile int*)&freed[sl] < seg) __nanosleep(64);
+                    if (lane == 0) {
+                        // a hand-over that never comes is a bug: trap instead of hanging the GPU
+                        for (unsigned spin = 0; *(volatile int*)&freed[sl] < seg; ++spin) {
+                            if (spin > (1u << 26)) __trap();
+                            __nanosleep(64);
+                        }
+                    }
                     __syncwarp();
                     __threadfence_block();
                     uint32_t* smem = g_dsmem + sl * SLOT;
@@ -1029,10 +1034,11 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 2) k_tc_pipe(KArgs a) {
             const int sl = seg & 1;
             bool go = false;
             if (lane == 0) {
-                while (true) {
+                for (unsigned spin = 0;; ++spin) {
                     if (*(volatile int*)&ready[sl] == seg) { go = true; break; }
                     const int tot = *(volatile int*)&nseg_total;
                     if (tot >= 0 && seg >= tot) break;
+                    if (spin > (1u << 27)) __trap();      // see the producer's wait
                     __nanosleep(32);
                 }
             }
