@@ -319,6 +319,20 @@ struct PolicySingle {       // one rank: X = {st == st_front(round)}; crossings 
             next[atomicAdd(next_count, 1)] = f;   // (warp-aggregating this append cost the decomposition 1 %)
         }
     }
+    // both survivors of a triangle: the two atomics in flight together (each
+    // returns the old support for the crossing test, so one after the other
+    // the second waited out the first's round trip)
+    __device__ __forceinline__ void dec2(int f, int g) const {
+        const uint32_t of = atomicSub(S + f, 1u), og = atomicSub(S + g, 1u);
+        if (of == thr) {
+            st[f] = st_front(round + 1);
+            next[atomicAdd(next_count, 1)] = f;
+        }
+        if (og == thr) {
+            st[g] = st_front(round + 1);
+            next[atomicAdd(next_count, 1)] = g;
+        }
+    }
 };
 
 // P owners of contiguous, word-aligned DAG-position slices (§8(e); the
@@ -341,6 +355,10 @@ struct PolicyPart {
     __device__ __forceinline__ int owner(int64_t e) const { return (int)(e / span); }
     __device__ __forceinline__ uint32_t live(int e) const { return S[(int64_t)owner(e) * stride + e]; }
     __device__ __forceinline__ bool in_x(int f) const { return (xbits[f >> 5] >> (f & 31)) & 1u; }
+    __device__ __forceinline__ void dec2(int f, int g) const {
+        dec(f);
+        dec(g);
+    }
     __device__ __forceinline__ void dec(int f) const {
         const int o = owner(f);
         if (me < 0 || o == me) {
@@ -356,8 +374,12 @@ template <class Pol>
 __device__ __forceinline__ void destroy(const Pol& pol, int e, int f, int g) {
     const bool fx = pol.in_x(f), gx = pol.in_x(g);
     if ((fx && f < e) || (gx && g < e)) return;   // a smaller X-edge owns this triangle
-    if (!fx) pol.dec(f);
-    if (!gx) pol.dec(g);
+    if (!fx && !gx) {
+        pol.dec2(f, g);
+    } else {
+        if (!fx) pol.dec(f);
+        if (!gx) pol.dec(g);
+    }
 }
 
 struct PeelArgs {
