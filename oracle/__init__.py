@@ -54,6 +54,9 @@ def _lib():
         L.or_truss_parallel.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p, i32p, u32p,
                                         i32p, i32p, ctypes.c_int]
         L.or_truss_parallel.restype = ctypes.c_int64
+        L.or_truss_parallel_ckpt.argtypes = [ctypes.c_int64, ctypes.c_int64, i32p, i32p, i64p, i32p, i32p, u32p,
+                                             i32p, i32p, ctypes.c_int, ctypes.c_char_p, ctypes.c_double]
+        L.or_truss_parallel_ckpt.restype = ctypes.c_int64
         _LIB = L
     return _LIB
 
@@ -163,21 +166,32 @@ class OracleGraph:
         return tau[: self.m].copy(), int(kmax.value)
 
     # O-8
-    def truss_parallel(self, support: np.ndarray | None = None, consume: bool = False):
+    def truss_parallel(self, support: np.ndarray | None = None, consume: bool = False, ckpt: str | None = None,
+                       budget_s: float = 0.0):
         """O-8: Alg. 4's incremental update element-wise, rounds parallel over
         the removed edges.  Uses the adjacency rows as scratch (copied unless
-        consume=True, which leaves this graph unusable)."""
+        consume=True, which leaves this graph unusable).  ckpt: resume from
+        that file if it exists; with budget_s > 0 the run saves its state
+        there at a level start once budget_s seconds have passed (after at
+        least one level) and returns None (call again to continue)."""
         if support is None:
             support = self.support()
         support = np.ascontiguousarray(support, dtype=np.uint32)
         col, eid = (self.col, self.eid) if consume else (self.col.copy(), self.eid.copy())
         tau = np.zeros(max(self.m, 1), dtype=np.int32)
         kmax = ctypes.c_int32(0)
-        r = _lib().or_truss_parallel(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p), _p(self.ptr, i64p),
-                                     _p(col, i32p), _p(eid, i32p), _p(support, u32p), _p(tau, i32p),
-                                     ctypes.byref(kmax), self.nthreads)
-        if r < 0:
-            raise MemoryError("or_truss_parallel: out of memory (or m > 2^31-1)")
+        r = _lib().or_truss_parallel_ckpt(self.n, self.m, _p(self.cu, i32p), _p(self.cv, i32p),
+                                          _p(self.ptr, i64p), _p(col, i32p), _p(eid, i32p), _p(support, u32p),
+                                          _p(tau, i32p), ctypes.byref(kmax), self.nthreads,
+                                          ckpt.encode() if ckpt else None, float(budget_s))
         if consume:
             self.col = self.eid = None
+        if r == -2:
+            return None                                   # saved to ckpt, unfinished
+        if r == -3:
+            raise ValueError(f"or_truss_parallel: unreadable checkpoint {ckpt}")
+        if r == -4:
+            raise OSError(f"or_truss_parallel: could not write checkpoint {ckpt}")
+        if r < 0:
+            raise MemoryError("or_truss_parallel: out of memory (or m > 2^31-1)")
         return tau[: self.m].copy(), int(kmax.value)

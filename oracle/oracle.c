@@ -40,6 +40,8 @@
 #include <string.h>
 #include <pthread.h>
 #include <unistd.h>
+#include <stdio.h>
+#include <time.h>
 
 static int n_threads(int t) {
     if (t > 0) return t;
@@ -643,9 +645,64 @@ static void o8_compact_rows(void* c, int64_t v0, int64_t v1, int t) {
     }
 }
 
+/* O-8 checkpoint (run-time bookkeeping only, no arithmetic): the state at a
+ * level start -- supports, edge states, trussness so far, k, kmax, rounds,
+ * live count.  The live list (alive edges in increasing id) and the rows
+ * (the adjacency without dead entries) are rebuilt from the states on resume;
+ * neither their order nor the compaction state changes any result. */
+typedef struct { int64_t magic, n, m, k, kmax, rounds, alive; } o8_ckpt_hdr;
+static const int64_t O8_MAGIC = 0x4f382d636b707431LL;
+
+static int o8_save(const char* path, int64_t n, int64_t m, int32_t k, int32_t kmax, int64_t rounds, int64_t alive,
+                   const uint32_t* S, const uint8_t* st, const int32_t* tau) {
+    char tmp[4096];
+    snprintf(tmp, sizeof tmp, "%s.part", path);
+    FILE* f = fopen(tmp, "wb");
+    if (!f) return -1;
+    o8_ckpt_hdr h = {O8_MAGIC, n, m, k, kmax, rounds, alive};
+    int ok = fwrite(&h, sizeof h, 1, f) == 1 && fwrite(S, 4, (size_t)m, f) == (size_t)m &&
+             fwrite(st, 1, (size_t)m, f) == (size_t)m && fwrite(tau, 4, (size_t)m, f) == (size_t)m;
+    ok = (fclose(f) == 0) && ok;
+    if (!ok || rename(tmp, path) != 0) return -1;
+    return 0;
+}
+
+static int o8_load(const char* path, int64_t n, int64_t m, int32_t* k, int32_t* kmax, int64_t* rounds, int64_t* alive,
+                   uint32_t* S, uint8_t* st, int32_t* tau) {
+    FILE* f = fopen(path, "rb");
+    if (!f) return 1;                                          /* no checkpoint: start */
+    o8_ckpt_hdr h;
+    int ok = fread(&h, sizeof h, 1, f) == 1 && h.magic == O8_MAGIC && h.n == n && h.m == m &&
+             fread(S, 4, (size_t)m, f) == (size_t)m && fread(st, 1, (size_t)m, f) == (size_t)m &&
+             fread(tau, 4, (size_t)m, f) == (size_t)m;
+    fclose(f);
+    if (!ok) return -1;
+    *k = (int32_t)h.k; *kmax = (int32_t)h.kmax; *rounds = h.rounds; *alive = h.alive;
+    return 0;
+}
+
+static double o8_now(void) {
+    struct timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return (double)t.tv_sec + 1e-9 * (double)t.tv_nsec;
+}
+
+int64_t or_truss_parallel_ckpt(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv, const int64_t* ptr,
+                               int32_t* col, int32_t* eid, const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out,
+                               int nthreads, const char* ckpt, double budget_s);
+
 int64_t or_truss_parallel(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv, const int64_t* ptr,
                           int32_t* col, int32_t* eid, const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out,
                           int nthreads) {
+    return or_truss_parallel_ckpt(n, m, cu, cv, ptr, col, eid, sup_init, tau, kmax_out, nthreads, NULL, 0.0);
+}
+
+/* ckpt (may be NULL): resume from that file if it exists; with budget_s > 0,
+ * after at least one level of this call and budget_s seconds, save the state
+ * there at the next level start and return -2 (unfinished). */
+int64_t or_truss_parallel_ckpt(int64_t n, int64_t m, const int32_t* cu, const int32_t* cv, const int64_t* ptr,
+                               int32_t* col, int32_t* eid, const uint32_t* sup_init, int32_t* tau, int32_t* kmax_out,
+                               int nthreads, const char* ckpt, double budget_s) {
     if (m == 0) { *kmax_out = 0; return 0; }
     if (m > INT32_MAX) return -1;
     const int T = n_threads(nthreads);
@@ -665,8 +722,31 @@ int64_t or_truss_parallel(int64_t n, int64_t m, const int32_t* cu, const int32_t
     for (int64_t e = 0; e < m; ++e) { S[e] = sup_init[e]; st[e] = 1; L[e] = (int32_t)e; tau[e] = 2; }
     for (int64_t v = 0; v < n; ++v) len[v] = ptr[v + 1] - ptr[v];
     int64_t nL = m, alive = m, compact_at = m, rounds = 0;
-    int32_t kmax = 2;
-    for (int32_t k = 3; alive > 0; ++k) {
+    int32_t kmax = 2, k0 = 3;
+    if (ckpt) {
+        const int r = o8_load(ckpt, n, m, &k0, &kmax, &rounds, &alive, S, st, tau);
+        if (r < 0) {
+            free(S); free(st); free(L); free(x); free(nx); free(len); free(kept); free(cnx); free(cmin);
+            return -3;                                         /* unreadable checkpoint */
+        }
+        if (r == 0) {                                          /* resume: live list and rows from the states */
+            nL = 0;
+            for (int64_t e = 0; e < m; ++e)
+                if (st[e]) L[nL++] = (int32_t)e;
+            o8_compact C = {ptr, len, col, eid, st};
+            parallel_for(n, T, o8_compact_rows, &C);
+            compact_at = alive;
+        }
+    }
+    const double t_start = o8_now();
+    int levels_here = 0;
+    for (int32_t k = k0; alive > 0; ++k) {
+        if (ckpt && budget_s > 0 && levels_here > 0 && o8_now() - t_start > budget_s) {
+            const int w = o8_save(ckpt, n, m, k, kmax, rounds, alive, S, st, tau);
+            free(S); free(st); free(L); free(x); free(nx); free(len); free(kept); free(cnx); free(cmin);
+            return w == 0 ? -2 : -4;                           /* unfinished (saved) / save failed */
+        }
+        ++levels_here;
         const uint32_t thr = (uint32_t)(k - 2);
         /* the level's first x; min s over the rest (empty-level skip); L keeps the alive edges */
         o8_scan Q = {L, nL, st, S, thr, T, nx, kept, cnx, cmin};

@@ -25,6 +25,7 @@ recorded: they are the full oracle runs the bench report quotes.
     python scripts/make_golden.py --crosscheck C4   (O-8 against an O-7 golden, from the cache)
     python scripts/make_golden.py --o4 C5           (O-4's triangle count against a golden's)
     python scripts/make_golden.py --support-only C5 (T and supports only: trussness_pending)
+    python scripts/make_golden.py --ckpt FILE SECONDS C5   (O-8 resumable: exit 3 = state saved, call again)
 
 GOLDEN_CACHE=<dir> overrides the cache directory (e.g. supports computed on
 one host, the trussness on another).
@@ -76,7 +77,8 @@ def hist(a: np.ndarray) -> dict:
     return {str(int(x)): int(c) for x, c in zip(vals, cnt)}
 
 
-def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only: bool = False) -> dict:
+def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only: bool = False,
+        ckpt: str | None = None, budget_s: float = 0.0) -> dict | None:
     os.makedirs(CACHE, exist_ok=True)
     cfg = gen.CONFIGS[name]
     times = {}
@@ -146,8 +148,18 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only:
         log(name, "O-7 kmax", kmax, f"{times['truss_sequential_s']:.1f}s")
     if tau_mode in ("o8", "both"):
         t = time.time()
-        tau8, kmax8 = g.truss_parallel(sup, consume=True)                  # O-8
-        times["truss_parallel_s"] = time.time() - t
+        res = g.truss_parallel(sup, consume=True, ckpt=ckpt, budget_s=budget_s)   # O-8
+        spent = time.time() - t
+        if ckpt:                                            # time over every resumed call
+            side = ckpt + ".time.json"
+            prev = json.load(open(side))["s"] if os.path.exists(side) else 0.0
+            json.dump({"s": prev + spent}, open(side, "w"))
+            spent += prev
+        if res is None:
+            log(name, f"O-8 unfinished after this call ({spent:.0f} s so far): state saved to {ckpt}")
+            return None
+        tau8, kmax8 = res
+        times["truss_parallel_s"] = spent
         log(name, "O-8 kmax", kmax8, f"{times['truss_parallel_s']:.1f}s")
         if tau_mode == "both":
             assert kmax8 == kmax and np.array_equal(tau8, tau), "O-7 and O-8 disagree"
@@ -227,6 +239,9 @@ def main(argv):
         return
     tau_mode = None
     support_only = False
+    ckpt, budget = None, 0.0
+    if argv and argv[0] == "--ckpt":                       # O-8 in several calls (C5 on a 1-hour host)
+        ckpt, budget, argv = argv[1], float(argv[2]), argv[3:]
     if argv and argv[0] == "--support-only":
         support_only, argv = True, argv[1:]
     if argv and argv[0] == "--tau":
@@ -234,7 +249,9 @@ def main(argv):
     names = argv or ["C3"]
     for name in names:
         ks = (3, 4, 5, 6) if name == "C3" else ()
-        d = run(name, ks, tau_mode or ("o8" if name == "C5" else "o7"), support_only)
+        d = run(name, ks, tau_mode or ("o8" if name == "C5" else "o7"), support_only, ckpt, budget)
+        if d is None:
+            sys.exit(3)
         path = os.path.join(GOLDEN, f"{name.lower()}_expected.json")
         with open(path, "w") as f:
             json.dump(d, f, indent=1, sort_keys=True)

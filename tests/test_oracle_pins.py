@@ -711,3 +711,24 @@ def test_tier2_decompositions_larger_graphs():
         assert np.array_equal(t8, tau) and k8 == kmax
         g1 = oracle.OracleGraph(u, v, nthreads=1)
         assert np.array_equal(g1.truss_parallel()[0], tau)
+
+
+def test_o8_checkpoint_resume(tmp_path):
+    """O-8 saved at every level start and resumed, call after call (the
+    run-time bookkeeping make_golden.py uses for C5), equals O-8 in one call
+    and O-6, the definition: the resumed live list and rows (rebuilt from the
+    saved edge states) change no result."""
+    u, v = gen.rmat(12, 16, 0.57, 0.19, 0.19, seed=5)
+    g = oracle.OracleGraph(u, v)
+    tau, kmax = g.truss_decomposition()
+    sup = g.support()
+    ck = str(tmp_path / "o8.ckpt")
+    calls, res = 0, None
+    while res is None:
+        gg = oracle.OracleGraph(u, v)                # a fresh process would rebuild the graph
+        res = gg.truss_parallel(sup, consume=True, ckpt=ck, budget_s=1e-9)
+        calls += 1
+    assert calls > 3                                  # it really stopped and resumed
+    assert np.array_equal(res[0], tau) and res[1] == kmax
+    one = oracle.OracleGraph(u, v).truss_parallel(sup)
+    assert np.array_equal(one[0], tau) and one[1] == kmax
