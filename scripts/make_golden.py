@@ -148,6 +148,8 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only:
         log(name, "O-7 kmax", kmax, f"{times['truss_sequential_s']:.1f}s")
     if tau_mode in ("o8", "both"):
         t = time.time()
+        if ckpt and os.environ.get("GOLDEN_DEADLINE"):     # budget up to a wall-clock deadline (epoch s)
+            budget_s = max(60.0, float(os.environ["GOLDEN_DEADLINE"]) - time.time())
         res = g.truss_parallel(sup, consume=True, ckpt=ckpt, budget_s=budget_s)   # O-8
         spent = time.time() - t
         if ckpt:                                            # time over every resumed call
