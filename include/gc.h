@@ -262,10 +262,6 @@ typedef enum gc_option {
                                  partitioned when there are several owners (NCCL ranks or
                                  loopback parts), 1 always (one owner included; testing),
                                  0 never (every rank builds the whole CSR) */
-    GC_OPT_PIPE = 21,         /* 1: the block-class (2) intersection kernels run pipelined -- two
-                                 head tables per 32-warp block, a producer warp building the next
-                                 head's table while 31 warps stream the current one (no
-                                 head-change barrier); 0 (default): k_tc_block */
 } gc_option;
 int gc_set_option(gc_ctx* ctx, int option, int64_t value);
 

@@ -580,9 +580,6 @@ int gc_set_option(gc_ctx* c, int option, int64_t value) {
             if (value < -1 || value > 1) return fail(c, GC_ERR_INVALID, "build partition mode must be -1, 0 or 1");
             c->build_part = (int)value;
             return GC_OK;
-        case GC_OPT_PIPE:
-            c->pipe = value ? 1 : 0;
-            return GC_OK;
         case GC_OPT_SORT_FRONT:
             if (value < 0 || value > ((int64_t)1 << 30)) return fail(c, GC_ERR_INVALID, "sort threshold out of range");
             c->sort_front = (int)value;

@@ -64,7 +64,7 @@ struct gc_ctx {
     cudaStream_t side = nullptr;     // library-owned side stream (warp-task classes overlap the block kernels)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int overlap = 1;                 // GC_OPT_OVERLAP
-    int launch_grid[6][2] = {};      // slots 0..4: classes; 5: the pipelined class-2 kernel      // intersection kernels: occupancy grid per class and SUP (0: not yet set up)
+    int launch_grid[5][2] = {};      // intersection kernels: occupancy grid per class and SUP (0: not yet set up)
     std::string err;
     bool poisoned = false;
     int state = 0;  // 0 created, 1 edges loaded, 2 graph built
@@ -153,7 +153,6 @@ struct gc_ctx {
     int64_t peel_big = getenv("GC_PEEL_BIG") ? atoll(getenv("GC_PEEL_BIG")) : INT64_MAX;
     int group_peel = 0;         // GC_OPT_GROUP_PEEL: frontier size from which a round groups its heavy edges (0: never)
     int group_heavy = 1024;     // GC_OPT_GROUP_HEAVY: shorter live row from which a frontier edge is grouped
-    int pipe = 0;               // GC_OPT_PIPE: class 2 through the pipelined (two-table, producer warp) kernel
     int sort_front = 1 << 20;   // GC_OPT_SORT_FRONT: frontiers of at least this many edges sorted by probed row (0: never)
     gcx::Buf alist;     // int32 live-edge list of the last compaction (level scans)
     int64_t alist_n = -1;       // -1: no list (scan every edge)

@@ -849,268 +849,6 @@ __global__ void k_fold_uw(uint32_t* __restrict__ sup, const uint16_t* __restrict
     }
 }
 
-// --------------------------------------- pipelined block-task kernel (2) --
-// The class-2 work of k_tc_block without its head-change barrier (ncu: 15 %
-// of the support kernel's warp samples wait there for the slowest of 16
-// warps).  A block of 32 warps holds TWO head tables.  Warp 0 is the
-// producer: it takes task batches from the global counter, cuts them into
-// segments (runs of tasks with one head) and builds segment i's table in
-// slot i & 1 while the 31 consumer warps stream segment i - 1 from the other
-// slot.  A consumer that finishes its share of a segment moves straight on to
-// the next one; the last consumer to finish a segment flushes its (v,w)
-// counters and empties the slot, which frees it for segment i + 2.  Slots
-// are handed over through shared-memory sequence numbers (producer: build,
-// fence, ready[s] = i; consumers: wait ready[s] == i, fence, read).
-constexpr int kPipeWarps = 32;
-constexpr int kPipeCons = kPipeWarps - 1;
-
-template <bool SUP>
-struct SmemBitmapSlot {                 // SmemBitmap at word offset off of the dynamic shared memory
-    static constexpr bool kBranchFree = true;
-    const uint32_t* bits;
-    const uint16_t* pre;
-    uint32_t* cnt;
-    uint32_t base;
-    uint32_t off;
-    __device__ __forceinline__ uint32_t hit(uint32_t w) const {
-        const uint32_t x = w - base;
-        const uint32_t word = g_dsmem[off + min(x >> 5, (uint32_t)(kBW - 1))];
-        return (word >> (x & 31)) & 1u;
-    }
-    __device__ __forceinline__ int loc(uint32_t w) const {
-        const uint32_t x = w - base;
-        const uint32_t word = g_dsmem[off + min(x >> 5, (uint32_t)(kBW - 1))];
-        return ((word >> (x & 31)) & 1u) ? (int)x : -1;
-    }
-    __device__ __forceinline__ void credit(int hd, uint32_t*) const {
-        if (!SUP) return;
-        const uint32_t x = (uint32_t)hd;
-        const uint64_t chunk = reinterpret_cast<const uint64_t*>(bits)[x >> 6];
-        const int j = (int)pre[x >> 6] + __popcll(chunk & ((1ull << (x & 63)) - 1ull));
-        atomicAdd(cnt + j, 1u);
-    }
-};
-
-struct PipeSeg {             // one published segment
-    int v, d, lg, use_bm;
-    long long r0, t0, t1;    // head row start; task range [t0, t1)
-};
-
-template <bool SUP>
-__global__ void __launch_bounds__(32 * kPipeWarps, 2) k_tc_pipe(KArgs a) {
-    constexpr int SLOT = SUP ? kBWS + kBW / 4 + kD2 : kBWS;   // words per slot (layout of k_tc_block)
-    __shared__ PipeSeg seg_desc[2];
-    __shared__ int ready[2], freed[2], done[2], nseg_total;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = threadIdx.x; j < 2 * SLOT; j += blockDim.x) g_dsmem[j] = 0u;   // tables empty
-    if (threadIdx.x < 2) {
-        ready[threadIdx.x] = -1;
-        freed[threadIdx.x] = threadIdx.x;   // slot s is free for segment s
-        done[threadIdx.x] = 0;
-    }
-    if (threadIdx.x == 0) nseg_total = -1;
-    __syncthreads();
-    uint32_t hits = 0;
-    if (warp == 0) {
-        // ------------------------------------------------------ producer
-        const int64_t nbatch = (a.ntask + a.batch - 1) / a.batch;
-        int seg = 0;
-        int64_t bt = blockIdx.x;
-        while (bt < nbatch) {
-            const int64_t tb0 = bt * a.batch, tb1 = min(a.ntask, (bt + 1) * a.batch);
-            // heads of the batch's tasks (-1: not owned), 32 at a time
-            for (int64_t base = tb0; base < tb1; base += 32) {
-                const int64_t t = base + lane;
-                int hv = -1;
-                if (t < tb1 && owned(a, t)) hv = __ldg(a.in_dst + (int)(uint32_t)a.tasks[t]);
-                // segment starts: owned tasks whose head differs from the previous owned task's
-                unsigned own = __ballot_sync(0xffffffffu, hv >= 0);
-                while (own) {
-                    const int s0 = __ffs(own) - 1;
-                    const int v = __shfl_sync(0xffffffffu, hv, s0);
-                    // extend over owned tasks of the same head (non-owned tasks are skipped by the consumers)
-                    const unsigned same = __ballot_sync(0xffffffffu, hv == v);
-                    const unsigned later = same & ~((1u << s0) - 1u);
-                    // the run ends at the first owned task of another head after s0
-                    const unsigned other = own & ~same & ~((1u << s0) - 1u);
-                    const int s1 = other ? __ffs(other) - 1 : 32;
-                    const unsigned mine = later & ((s1 == 32) ? 0xffffffffu : ((1u << s1) - 1u));
-                    own &= ~mine;
-                    // wait for the slot, then build segment seg's table in it
-                    const int sl = seg & 1;
-                    if (lane == 0) {
-                        // a hand-over that never comes is a bug: trap instead of hanging the GPU
-                        for (unsigned spin = 0; *(volatile int*)&freed[sl] < seg; ++spin) {
-                            if (spin > (1u << 26)) __trap();
-                            __nanosleep(64);
-                        }
-                    }
-                    __syncwarp();
-                    __threadfence_block();
-                    uint32_t* smem = g_dsmem + sl * SLOT;
-                    uint32_t* bits = smem;
-                    uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);
-                    uint32_t* bcnt = smem + kBWS + kBW / 4;
-                    uint32_t* keys = smem;
-                    int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
-                    uint32_t* hcnt = smem + kBWS;
-                    const int64_t r0 = __ldg(a.dag_ptr + v);
-                    const int d = (int)(__ldg(a.dag_ptr + v + 1) - r0);
-                    const uint32_t span = (uint32_t)__ldg(a.dag_col + r0 + d - 1) - (uint32_t)v;
-                    const bool use_bm = span <= a.bm_bits;
-                    int lg = 0;
-                    if (use_bm) {
-                        // four rows' loads in flight per lane, then the inserts; the previous
-                        // entry of lane 0's element comes from lane 31 of the step before
-                        uint32_t carry = 0xFFFFFFFFu;   // window offset of entry j0 - 1 (none before 0)
-                        for (int j0 = 0; j0 < d; j0 += 128) {
-                            uint32_t x[4];
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int j = j0 + 32 * k + lane;
-                                x[k] = j < d ? (uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u : 0xFFFFFFFFu;
-                            }
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int j = j0 + 32 * k + lane;
-                                uint32_t prev = __shfl_up_sync(0xffffffffu, x[k], 1);
-                                const uint32_t last = __shfl_sync(0xffffffffu, x[k], 31);
-                                if (lane == 0) prev = carry;
-                                carry = last;
-                                if (j < d) {
-                                    atomicOr(bits + (x[k] >> 5), 1u << (x[k] & 31));
-                                    if (SUP) {
-                                        bcnt[j] = 0u;
-                                        if (j == 0 || (prev >> 6) != (x[k] >> 6)) pre[x[k] >> 6] = (uint16_t)j;
-                                    }
-                                }
-                            }
-                        }
-                    } else {
-                        lg = table_lg(d, __builtin_ctz(kTS2));
-                        const int ts = 1 << lg;
-                        for (int j = lane; j < ts; j += 32) {
-                            keys[j] = kEmpty;
-                            if (SUP) hcnt[j] = 0;
-                        }
-                        __syncwarp();
-                        for (int j = lane; j < d; j += 32) {
-                            const uint32_t w = (uint32_t)__ldg(a.dag_col + r0 + j);
-                            uint32_t h = hash_slot(w, lg);
-                            while (atomicCAS(keys + h, kEmpty, w) != kEmpty) h = (h + 1) & (ts - 1);
-                            if (SUP) vals[h] = j;
-                        }
-                    }
-                    __syncwarp();
-                    __threadfence_block();
-                    if (lane == 0) {
-                        volatile PipeSeg* ds = &seg_desc[sl];
-                        ds->v = v;
-                        ds->d = d;
-                        ds->lg = lg;
-                        ds->use_bm = use_bm;
-                        ds->r0 = r0;
-                        ds->t0 = base + s0;
-                        ds->t1 = base + ((s1 == 32) ? min((int64_t)32, tb1 - base) : s1);
-                        __threadfence_block();
-                        *(volatile int*)&ready[sl] = seg;
-                    }
-                    __syncwarp();
-                    ++seg;
-                }
-            }
-            bt = a.next ? (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu,
-                                                                   lane == 0 ? (long long)atomicAdd(a.next, 1ull) : 0ll, 0)
-                        : bt + gridDim.x;
-        }
-        if (lane == 0) {
-            __threadfence_block();
-            *(volatile int*)&nseg_total = seg;
-        }
-    } else {
-        // ------------------------------------------------------ consumers
-        const int cw = warp - 1;
-        for (int seg = 0;; ++seg) {
-            const int sl = seg & 1;
-            bool go = false;
-            if (lane == 0) {
-                for (unsigned spin = 0;; ++spin) {
-                    if (*(volatile int*)&ready[sl] == seg) { go = true; break; }
-                    const int tot = *(volatile int*)&nseg_total;
-                    if (tot >= 0 && seg >= tot) break;
-                    if (spin > (1u << 27)) __trap();      // see the producer's wait
-                    __nanosleep(32);
-                }
-            }
-            if (!__shfl_sync(0xffffffffu, go, 0)) break;
-            __threadfence_block();
-            const volatile PipeSeg* ds = &seg_desc[sl];
-            const int v = ds->v, d = ds->d, lg = ds->lg;
-            const bool use_bm = ds->use_bm;
-            const int64_t r0 = ds->r0, t0 = ds->t0, t1 = ds->t1;
-            uint32_t* smem = g_dsmem + sl * SLOT;
-            uint32_t* bits = smem;
-            uint16_t* pre = reinterpret_cast<uint16_t*>(smem + kBWS);
-            uint32_t* bcnt = smem + kBWS + kBW / 4;
-            uint32_t* keys = smem;
-            int32_t* vals = reinterpret_cast<int32_t*>(smem + kTS2);
-            uint32_t* hcnt = smem + kBWS;
-            for (int64_t t = t0; t < t1; ++t) {
-                if (!owned(a, t)) continue;
-                const uint64_t pk = a.tasks[t];
-                const int i0 = (int)(uint32_t)pk, i1 = (int)(pk >> 32);
-                const int64_t c0 = __ldg(a.in_cost + i0), c1 = __ldg(a.in_cost + i1);
-                const int64_t ca = c0 + (c1 - c0) * cw / kPipeCons, cb = c0 + (c1 - c0) * (cw + 1) / kPipeCons;
-                if (cb <= ca) continue;
-                const int first = (int)warp_lower_bound(a.in_cost, i0, i1, ca + 1, lane) - 1;
-                const int end = (int)warp_lower_bound(a.in_cost, i0, i1, cb, lane);
-                if (use_bm) {
-                    SmemBitmapSlot<SUP> B{bits, pre, bcnt, (uint32_t)v + 1u, (uint32_t)(sl * SLOT)};
-                    hits += stream_task<SUP, true>(first, end, c0, (int)(ca - c0), (int)(cb - c0), a.in_pos, a.in_src,
-                                                   a.in_cost, a.dag_ptr, a.dag_col, a.sup, a.uw16, B, lane,
-                                                   a.long_seg, a.uw);
-                } else {
-                    SmemHash<SUP> H{keys, vals, hcnt, lg, (uint32_t)((1 << lg) - 1)};
-                    hits += stream_task<SUP, true>(first, end, c0, (int)(ca - c0), (int)(cb - c0), a.in_pos, a.in_src,
-                                                   a.in_cost, a.dag_ptr, a.dag_col, a.sup, a.uw16, H, lane,
-                                                   a.long_seg, a.uw);
-                }
-            }
-            // arrive; the last consumer flushes and empties the slot
-            __syncwarp();
-            int last = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                last = atomicAdd(&done[sl], 1) == kPipeCons - 1;
-            }
-            if (__shfl_sync(0xffffffffu, last, 0)) {
-                __threadfence_block();
-                if (use_bm) {
-                    for (int j = lane; j < d; j += 32) {
-                        if (SUP && bcnt[j]) atomicAdd(a.sup + r0 + j, bcnt[j]);
-                        bits[((uint32_t)__ldg(a.dag_col + r0 + j) - (uint32_t)v - 1u) >> 5] = 0u;
-                    }
-                } else {
-                    const int ts = 1 << lg;
-                    for (int j = lane; j < ts; j += 32) {
-                        if (SUP && hcnt[j]) atomicAdd(a.sup + r0 + vals[j], hcnt[j]);
-                        keys[j] = 0u;
-                        vals[j] = 0;
-                    }
-                }
-                __syncwarp();
-                __threadfence_block();
-                if (lane == 0) {
-                    done[sl] = 0;
-                    __threadfence_block();
-                    *(volatile int*)&freed[sl] = seg + 2;
-                }
-            }
-        }
-    }
-    add_count(a.count, hits, lane);
-}
-
 template <class T>
 __global__ void k_scatter_t(const T* __restrict__ vals, const int32_t* __restrict__ eid, int64_t m,
                             T* __restrict__ out) {
@@ -1333,22 +1071,7 @@ static int launch_classes(gc_ctx* c, int owner, int parts, unsigned long long* c
             GC_LAUNCH(c, (k_tc_block<SUP, false>), (int)std::min<int64_t>({grid, a.ntask, 4096}), threads, smem, a);
         }
     }
-    if (c->ntask[2] > 0 && c->pipe) {
-        // class 2 through the pipelined kernel (two head tables per block, producer warp)
-        a.next = GC_DYN_BATCH ? next + 1 : nullptr;
-        a.slot = nullptr;
-        a.tasks = tasks + c->task_off[2];
-        a.ntask = c->ntask[2];
-        a.task_pref = parts > 1 ? c->task_pref.as<int64_t>() + c->task_off[2] : nullptr;
-        a.cls_start = c->cls_start[2];
-        a.cls_total = c->cls_total[2];
-        const size_t smem = (size_t)2 * (SUP ? kBWS + kBW / 4 + kD2 : kBWS) * sizeof(uint32_t);
-        constexpr int threads = 32 * kPipeWarps;
-        const int grid = prep(5, k_tc_pipe<SUP>, smem, threads);
-        if (grid < 0) return cuda_fail(c, cudaGetLastError(), "cudaFuncSetAttribute(k_tc_pipe)", __FILE__, __LINE__);
-        const int64_t nb = (a.ntask + a.batch - 1) / a.batch;
-        GC_LAUNCH(c, (k_tc_pipe<SUP>), (int)std::min<int64_t>({grid, nb, 4096}), threads, smem, a);
-    } else if (c->ntask[2] > 0) {
+    if (c->ntask[2] > 0) {
         a.next = GC_DYN_BATCH ? next + 1 : nullptr;
         a.slot = slots + 2 * 4096;
         a.tasks = tasks + c->task_off[2];

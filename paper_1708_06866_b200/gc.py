@@ -46,7 +46,6 @@ GC_OPT_OVERLAP = 13
 GC_OPT_WORK_STATS = 15
 GC_OPT_BUILD_PART = 16
 GC_OPT_SORT_FRONT = 18
-GC_OPT_PIPE = 21
 
 # Every symbol include/gc.h declares (checked by tests/test_abi.py).
 EXPORTS = [
