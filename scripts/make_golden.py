@@ -158,7 +158,10 @@ def run(name: str, ktruss_batch: tuple = (), tau_mode: str = "o7", support_only:
             json.dump({"s": prev + spent}, open(side, "w"))
             spent += prev
         if res is None:
-            log(name, f"O-8 unfinished after this call ({spent:.0f} s so far): state saved to {ckpt}")
+            hdr = np.fromfile(ckpt, dtype=np.int64, count=7)    # magic, n, m, k, kmax, rounds, alive
+            log(name, f"O-8 unfinished after this call ({spent:.0f} s so far): state saved to {ckpt} "
+                      f"at level k={int(hdr[3])}, kmax so far {int(hdr[4])}, rounds {int(hdr[5])}, "
+                      f"live edges {int(hdr[6])} of {g.m}")
             return None
         tau8, kmax8 = res
         times["truss_parallel_s"] = spent
