@@ -448,6 +448,21 @@ __device__ __forceinline__ void lower_bound_x2(const int32_t* __restrict__ a, in
     r1 = p1 + (__ldg(a + p1) < x1);
 }
 
+#ifndef GC_PEEL_PF
+#define GC_PEEL_PF 0            // TMA bulk L2 prefetch (cp.async.bulk.prefetch.L2) of the next warp-walked edge's rows
+#endif
+#ifndef GC_PEEL_PF_MAX
+#define GC_PEEL_PF_MAX 2048     // ... the searched (longer) row only up to this many entries
+#endif
+#if GC_PEEL_PF
+// a[lo, hi) into L2 through the TMA unit (16-byte aligned superset; warp-uniform arguments)
+__device__ __forceinline__ void row_pf(const int32_t* __restrict__ a, int64_t lo, int64_t hi) {
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a + lo) & ~(uintptr_t)15;
+    const uintptr_t z = (reinterpret_cast<uintptr_t>(a + hi) + 15) & ~(uintptr_t)15;
+    if (hi > lo) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x), "r"((uint32_t)(z - x)) : "memory");
+}
+#endif
+
 template <class Pol>
 __device__ __forceinline__ void peel_one_warp(const PeelArgs& A, const Pol& pol, int e, uint32_t live, int64_t a0,
                                               int64_t a1, int64_t b0, int64_t b1, int lane) {
@@ -599,6 +614,19 @@ __global__ void __launch_bounds__(256, MINB) k_peel(PeelArgs A, Pol pol) {
         while (coop) {                                  // the whole warp, one edge at a time
             const int src = __ffs(coop) - 1;
             coop &= coop - 1;
+#if GC_PEEL_PF
+            if (coop) {   // TMA bulk L2 prefetch of the next edge's rows while this one is walked
+                const int nx = __ffs(coop) - 1;
+                const int64_t na0 = __shfl_sync(0xffffffffu, a0, nx), na1 = __shfl_sync(0xffffffffu, a1, nx);
+                const int64_t nb0 = __shfl_sync(0xffffffffu, b0, nx), nb1 = __shfl_sync(0xffffffffu, b1, nx);
+                if (lane == 0) {
+                    const int64_t t0 = max(na0, na1 - 64);   // the walk's first chunks, from the row end
+                    row_pf(A.sym_col, t0, na1);
+                    row_pf(A.sym_eid, t0, na1);
+                    if (nb1 - nb0 <= GC_PEEL_PF_MAX) row_pf(A.sym_col, nb0, nb1);   // the searched row, whole
+                }
+            }
+#endif
             peel_one_warp<Pol>(A, pol, __shfl_sync(0xffffffffu, e, src), __shfl_sync(0xffffffffu, live, src),
                           __shfl_sync(0xffffffffu, a0, src), __shfl_sync(0xffffffffu, a1, src),
                           __shfl_sync(0xffffffffu, b0, src), __shfl_sync(0xffffffffu, b1, src), lane);
@@ -959,8 +987,8 @@ int build_sym(gc_ctx* c) {
     if (c->sym_ready) return GC_OK;
     const int64_t n = c->n, m = c->m;
     GC_TRY(ensure(c, c->sym_ptr, (size_t)(n + 1) * 8));
-    GC_TRY(ensure(c, c->sym_col, (size_t)2 * m * 4));
-    GC_TRY(ensure(c, c->sym_eid, (size_t)2 * m * 4));
+    GC_TRY(ensure(c, c->sym_col, (size_t)2 * m * 4 + 64));   // +64: 16-byte aligned bulk prefetches
+    GC_TRY(ensure(c, c->sym_eid, (size_t)2 * m * 4 + 64));
     GC_TRY(ensure(c, c->live_len, (size_t)n * 4));
     GC_TRY(ensure(c, c->long_rows, (size_t)n * 4));
     GC_LAUNCH(c, k_sym_ptr, grid_for(n + 1), kThreads, 0, c->dag_ptr.as<int64_t>(), c->in_ptr.as<int64_t>(), n,

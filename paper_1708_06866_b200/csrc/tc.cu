@@ -53,6 +53,11 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
                            // pass 99.8 -> 95.3 / 1,282 -> 1,122 ms); 0: one 32-bit atomic per credit
 #endif
 constexpr int kOvh = GC_KOVH;               // per in-edge overhead in the cost model (cost units)
+#ifndef GC_BULK_PF
+#define GC_BULK_PF 0       // TMA bulk L2 prefetch of the streamed suffixes (cp.async.bulk.prefetch.L2): 1 = each
+                           // long suffix whole when the warp starts it, plus the next long one; 2 = also every
+                           // short suffix of a 32-in-edge group (per-lane addresses: a uniform-register loop)
+#endif
 #ifndef GC_KD1
 #define GC_KD1 128
 #endif
@@ -254,6 +259,19 @@ __device__ __forceinline__ void credit_uw(uint32_t* __restrict__ sup, uint16_t* 
     credit_u(sup, uw16, q, 1u);
 }
 
+#if GC_BULK_PF
+// TMA bulk prefetch of dag_col[beg, beg + len) into L2 (16-byte aligned
+// superset; dag_col carries 64 bytes of padding past its end).  The operands of
+// UBLKPF are uniform registers: call it with warp-uniform arguments, or the
+// compiler loops over the lanes' distinct addresses.
+__device__ __forceinline__ void bulk_pf(const int32_t* __restrict__ col, int beg, int len) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(col + beg) & ~(uintptr_t)15;
+    const uintptr_t z = (reinterpret_cast<uintptr_t>(col + beg + len) + 15) & ~(uintptr_t)15;
+    if (z > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(z - a)) : "memory");
+}
+#endif
+
 // ------------------------------------------------------- stream routine --
 // Walk the suffixes of the in-edges [i0, i1), 32 in-edges per group,
 // flattening their wedges across the 32 lanes so short and long suffixes
@@ -292,14 +310,31 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                 len = hi - lo;
             }
         }
+#if GC_BULK_PF >= 2
+        if (len > 0 && len < long_seg) bulk_pf(dag_col, beg, len);
+#endif
         // Long suffixes (the bulk of the wedges): one at a time with the whole
         // warp, 16-byte vector loads, no segment search.
         unsigned longs = __ballot_sync(0xffffffffu, len >= long_seg);
+#if GC_BULK_PF >= 1
+        if (longs) {
+            const int s0 = __ffs(longs) - 1;
+            const int b0 = __shfl_sync(0xffffffffu, beg, s0), l0 = __shfl_sync(0xffffffffu, len, s0);
+            if (lane == 0) bulk_pf(dag_col, b0, l0);
+        }
+#endif
         while (longs) {
             const int s = __ffs(longs) - 1;
             longs &= longs - 1;
             const int b = __shfl_sync(0xffffffffu, beg, s);
             const int e = b + __shfl_sync(0xffffffffu, len, s);
+#if GC_BULK_PF >= 1
+            if (longs) {   // the next long suffix streams into L2 while this one is probed
+                const int s1 = __ffs(longs) - 1;
+                const int b1 = __shfl_sync(0xffffffffu, beg, s1), l1 = __shfl_sync(0xffffffffu, len, s1);
+                if (lane == 0) bulk_pf(dag_col, b1, l1);
+            }
+#endif
             uint32_t seg_hits = 0;
             auto visit = [&](int q, int w) {
                 const uint32_t inr = (uint32_t)(q - b) < (uint32_t)(e - b);
