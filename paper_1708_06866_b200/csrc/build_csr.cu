@@ -583,7 +583,6 @@ static int part_orient(gc_ctx* c, int64_t n, int b, int64_t m) {
     int64_t cut[65], base[65];
     GC_TRY(owner_cuts(c, dptr, n, P, cut, base));
     int64_t* d_nsel = reinterpret_cast<int64_t*>(c->scal.as<char>() + 968);
-    int64_t* h = static_cast<int64_t*>(c->hpin);
     int32_t* sel = c->vals_a.as<int32_t>();
     uint64_t* ka = c->keys_a.as<uint64_t>();
     uint64_t* kb = c->keys_b.as<uint64_t>();
@@ -602,7 +601,6 @@ static int part_orient(gc_ctx* c, int64_t n, int b, int64_t m) {
                   c->dag_src.as<int32_t>() + base[r]);
         GC_TRY(tm.end(r));
     }
-    (void)h;
     if (nccl) {
         int64_t counts[64], offs[64];
         for (int r = 0; r < P; ++r) {
@@ -697,7 +695,6 @@ int build_csr(gc_ctx* c) {
     c->n = n;
     const int b = n > 1 ? ceil_log2_u64((uint64_t)n) : 1;
     c->bits = b;
-    const uint64_t mask = (1ULL << b) - 1;
 
     // ---- a2: pack, sort, unique
     int64_t m = 0;

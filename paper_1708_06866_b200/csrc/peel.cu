@@ -895,17 +895,9 @@ __global__ void k_pivot_keys(const int32_t* __restrict__ front, int nf, const in
     }
 }
 
-__global__ void k_finish_round(const int32_t* __restrict__ front, int nfront, uint8_t* __restrict__ alive,
-                               int32_t* __restrict__ tau, int32_t level) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nfront; i += gridDim.x * blockDim.x) {
-        int e = front[i];
-        alive[e] = 0;
-        if (tau) tau[e] = level;
-    }
-}
-
-// k_finish_round for a frontier whose size is on the device; also counts the
-// removed edges and the non-empty rounds
+// End of a round: the frontier (its size on the device) leaves the alive set
+// (tau = level in a decomposition); also counts the removed edges and the
+// non-empty rounds
 __global__ void k_finish_round_dev(const int32_t* __restrict__ front, const int* __restrict__ nfront_dev,
                                    uint8_t* __restrict__ alive, int32_t* __restrict__ tau, int32_t level,
                                    unsigned long long* __restrict__ acc) {

@@ -54,9 +54,10 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 #endif
 constexpr int kOvh = GC_KOVH;               // per in-edge overhead in the cost model (cost units)
 #ifndef GC_BULK_PF
-#define GC_BULK_PF 0       // TMA bulk L2 prefetch of the streamed suffixes (cp.async.bulk.prefetch.L2): 1 = each
-                           // long suffix whole when the warp starts it, plus the next long one; 2 = also every
-                           // short suffix of a 32-in-edge group (per-lane addresses: a uniform-register loop)
+#define GC_BULK_PF 0       // TMA bulk L2 prefetch (cp.async.bulk.prefetch.L2), bit mask: 1 = each long suffix
+                           // whole when the warp starts it, plus the next long one; 2 = every short suffix of a
+                           // 32-in-edge group (per-lane addresses: a uniform-register loop); 4 = the next group's
+                           // in-edge records (in_pos, in_src, in_cost)
 #endif
 #ifndef GC_KD1
 #define GC_KD1 128
@@ -294,6 +295,14 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
     for (int base = i0; base < i1; base += 32) {
         const int i = base + lane;
         const bool valid = i < i1;
+#if GC_BULK_PF & 4
+        if (lane == 0 && base + 32 < i1) {   // the next group's in-edge records
+            const int nb = base + 32, ne = min(i1, base + 64);
+            bulk_pf(in_pos, nb, ne - nb);
+            bulk_pf(in_src, nb, ne - nb);
+            if (CLIP) bulk_pf(reinterpret_cast<const int32_t*>(in_cost), 2 * nb, 2 * (ne - nb));
+        }
+#endif
         int p = 0, beg = 0, len = 0;
         if (valid) {
             p = __ldg(in_pos + i);
@@ -310,13 +319,13 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
                 len = hi - lo;
             }
         }
-#if GC_BULK_PF >= 2
+#if GC_BULK_PF & 2
         if (len > 0 && len < long_seg) bulk_pf(dag_col, beg, len);
 #endif
         // Long suffixes (the bulk of the wedges): one at a time with the whole
         // warp, 16-byte vector loads, no segment search.
         unsigned longs = __ballot_sync(0xffffffffu, len >= long_seg);
-#if GC_BULK_PF >= 1
+#if GC_BULK_PF & 1
         if (longs) {
             const int s0 = __ffs(longs) - 1;
             const int b0 = __shfl_sync(0xffffffffu, beg, s0), l0 = __shfl_sync(0xffffffffu, len, s0);
@@ -328,7 +337,7 @@ __device__ __forceinline__ uint32_t stream_task(int i0, int i1, int64_t cbase, i
             longs &= longs - 1;
             const int b = __shfl_sync(0xffffffffu, beg, s);
             const int e = b + __shfl_sync(0xffffffffu, len, s);
-#if GC_BULK_PF >= 1
+#if GC_BULK_PF & 1
             if (longs) {   // the next long suffix streams into L2 while this one is probed
                 const int s1 = __ffs(longs) - 1;
                 const int b1 = __shfl_sync(0xffffffffu, beg, s1), l1 = __shfl_sync(0xffffffffu, len, s1);
