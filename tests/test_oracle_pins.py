@@ -732,3 +732,46 @@ def test_o8_checkpoint_resume(tmp_path):
     assert np.array_equal(res[0], tau) and res[1] == kmax
     one = oracle.OracleGraph(u, v).truss_parallel(sup)
     assert np.array_equal(one[0], tau) and one[1] == kmax
+
+
+def test_trussness_h_index_identity():
+    """Pin of O-6 / O-7 / O-8 from the definitions alone:
+    kappa = tau - 2 is a fixed point of kappa(e) = H({min(kappa(f), kappa(g))})
+    over the triangles (e, f, g), H the h-index (tests/truss_props.py: soundness
+    one way, maximality the other) - checked on every edge of C1, a skewed
+    R-MAT and a hub graph; and the checker rejects a trussness raised or
+    lowered on one edge (it is what test_c5_full applies to the GPU's tau)."""
+    import truss_props as tp
+    hub_u = np.r_[np.zeros(400, np.int32), np.arange(1, 40, dtype=np.int32)]
+    hub_v = np.r_[np.arange(1, 401, dtype=np.int32), np.arange(2, 41, dtype=np.int32)]
+    graphs = [gen.CONFIGS["C1"].generate(), gen.rmat(11, 16, 0.65, 0.15, 0.15, seed=8), (hub_u, hub_v)]
+    for u, v in graphs:
+        g = oracle.OracleGraph(u, v)
+        sup = g.support()
+        for tau, kmax in (g.truss_decomposition(), g.truss_parallel(), g.truss_sequential()):
+            tp.check_global(sup, tau, kmax)
+            assert tp.check_local(g.ptr, g.col, g.eid, g.cu, g.cv, tau, np.arange(g.m)) == g.m
+    # the checker's own teeth, on the last graphs' trussness
+    u, v = graphs[0]
+    g = oracle.OracleGraph(u, v)
+    sup = g.support()
+    tau, kmax = g.truss_decomposition()
+    rng = np.random.default_rng(4)
+    for delta in (+1, -1):
+        caught = 0
+        cand = np.flatnonzero(tau > 3)
+        for e in rng.choice(cand, size=40, replace=False):
+            bad = tau.copy()
+            bad[e] += delta
+            try:
+                tp.check_local(g.ptr, g.col, g.eid, g.cu, g.cv, bad, np.array([e]))
+            except AssertionError:
+                caught += 1
+        assert caught == 40, (delta, caught)
+    # sampling covers every populated level
+    s = tp.sample_edges(tau, 100, 10, 2, seed=1)
+    assert set(np.unique(tau[s])) == set(np.unique(tau))
+    bad = tau.copy()
+    bad[np.flatnonzero(sup == 0)[0]] = 3
+    with pytest.raises(AssertionError):
+        tp.check_global(sup, bad, kmax)

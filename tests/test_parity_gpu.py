@@ -295,7 +295,28 @@ def hist(a):
     return {str(int(x)): int(c) for x, c in zip(vals, cnt)}
 
 
-def check_golden(c, d, ks=(3, 4, 5, 6), fused_k=None):
+def check_trussness_properties(c, d, sup, adj, n_uniform=3000, n_top=500, per_level=1):
+    """The decomposition against what holds at any size (tests/truss_props.py):
+    the 3-truss mask is {s >= 1} of the golden-checked supports, tau = 2 exactly
+    there, tau <= s + 2, kmax = max tau, and on a seeded sample (uniform edges,
+    the deepest edges, one edge of every level) the h-index identity
+    kappa(e) = H({min(kappa(f), kappa(g))}) - soundness and maximality of every
+    level at that edge.  `adj` is the oracle's adjacency
+    (rows with edge ids) of the same input."""
+    import truss_props as tp
+    assert np.array_equal(adj.cu, c.get_edges()[0])
+    mask, m_alive = c.ktruss(3)
+    assert m_alive == d["m"] - d["support_zero"] and np.array_equal(mask.astype(bool), sup > 0)
+    del mask
+    tau, kmax = c.truss_decomposition()
+    tp.check_global(sup, tau, kmax)
+    edges = tp.sample_edges(tau, n_uniform, n_top, per_level, seed=d["m"] % 1000)
+    n = tp.check_local(adj.ptr, adj.col, adj.eid, adj.cu, adj.cv, tau, edges)
+    assert n >= min(n_uniform // 2, tau.size)
+    return tau, kmax
+
+
+def check_golden(c, d, ks=(3, 4, 5, 6), fused_k=None, adj=None):
     """Every result of one built context against the oracle's golden file:
     canonical edge list, T, supports, k-truss masks, trussness and kmax
     (sha256 of the canonical-order arrays, plus histograms)."""
@@ -310,8 +331,12 @@ def check_golden(c, d, ks=(3, 4, 5, 6), fused_k=None):
     assert int(sup.max(initial=0)) == d["support_max"] and int((sup == 0).sum()) == d["support_zero"]
     assert sha(sup) == d["support_sha256"]
     if d.get("trussness_pending"):
-        # the golden holds T and supports only (scripts/make_golden.py --support-only)
-        pytest.xfail("trussness golden not generated for this config (O-8 takes hours); T and supports equal")
+        # the golden holds T and supports only (scripts/make_golden.py --support-only): the
+        # decomposition is checked by its size-independent properties, then the missing exact
+        # comparison is reported as an expected failure
+        tau, kmax = check_trussness_properties(c, d, sup, adj)
+        pytest.xfail(f"no exact trussness golden for this config (O-8 takes hours); T, every support and the "
+                     f"trussness properties hold (kmax {kmax}, {np.unique(tau).size} levels)")
     for k in ks:
         mask, m_alive = c.ktruss(k)
         assert m_alive == d["ktruss_size"][str(k)], k
@@ -332,7 +357,7 @@ def check_golden(c, d, ks=(3, 4, 5, 6), fused_k=None):
         assert sha((tau >= k).astype(np.uint8)) == d["ktruss_sha256"][str(k)]
 
 
-def run_config_golden(gcmod, name, **kw):
+def run_config_golden(gcmod, name, props=False, **kw):
     """Full-size config in bench.py's launch configuration (torch's current
     stream, device-resident raw lists)."""
     import torch
@@ -342,9 +367,12 @@ def run_config_golden(gcmod, name, **kw):
     c = gcmod.Context(0, torch.cuda.current_stream())
     try:
         c.load_edges(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda())
+        adj = oracle.OracleGraph(u, v) if (props or d.get("trussness_pending")) else None
         del u, v
         c.build_csr()
-        check_golden(c, d, **kw)
+        check_golden(c, d, adj=adj, **kw)
+        if props and not d.get("trussness_pending"):   # the checker accepts an exact decomposition at size
+            check_trussness_properties(c, d, c.edge_support(), adj)
     finally:
         c.close()
 
@@ -353,7 +381,7 @@ def test_c3_full(gcmod):
     """BASELINE configs[2] (R-MAT s20): T, every support, the k-truss masks at
     k = 3, 4, 5, 6 (O-5, the definition) and the full trussness
     (O-7, equal to O-5's masks as tau >= k) — exact, every edge."""
-    run_config_golden(gcmod, "C3", fused_k=4)
+    run_config_golden(gcmod, "C3", fused_k=4, props=True)
 
 
 def test_c4_full(gcmod):
