@@ -86,6 +86,9 @@ def main():
         dseq = launches(dec_path)
         j = next(i for i, k in enumerate(dseq) if sup_flag(k["name"]) is True)
         summ["decomposition"] = seg_sum(dseq[j:])
+        dec_seq = dseq[j:]
+    else:
+        dec_seq = None
     for key in list(summ):
         if isinstance(summ[key], dict) and "dram_bytes" in summ[key]:
             summ[key]["dram_bytes_per_launch"] = summ[key]["dram_bytes"]
@@ -108,6 +111,10 @@ def main():
         f.write("\n`ktruss` = every kernel of the gc_ktruss_analysis(4) call (support pass, output scatter, "
                 "level scan, symmetric rows, peel rounds); `decomposition` = every kernel of one "
                 "gc_truss_decomposition call after its support pass's first kernel (scripts/run_decomp.py).\n")
+        if dec_seq:
+            dms = sum(k.get("gpu__time_duration.sum", 0) for k in dec_seq)
+            f.write(f"\n## gc_truss_decomposition — {dms:.1f} ms of kernels, {len(dec_seq)} launches\n\n")
+            table(f, dec_seq, dms)
     # --set full reports
     names = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
              "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__inst_issued.avg.pct_of_peak_sustained_active",
