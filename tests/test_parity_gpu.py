@@ -335,6 +335,17 @@ def check_golden(c, d, ks=(3, 4, 5, 6), fused_k=None, adj=None):
         # decomposition is checked by its size-independent properties, then the missing exact
         # comparison is reported as an expected failure
         tau, kmax = check_trussness_properties(c, d, sup, adj)
+        part = d.get("trussness_partial")
+        if part:
+            # O-8 finished every level below clip + 1 before its deadline: min(trussness, clip) is exact
+            clip = np.minimum(tau, np.int32(part["clip"])).astype(np.int32)
+            assert kmax >= part["kmax_at_least"]
+            assert int((tau >= part["clip"]).sum()) == part["live_edges"]
+            assert hist(clip) == part["clip_hist"]
+            assert sha(clip) == part["clip_sha256"]
+            pytest.xfail(f"exact trussness golden only below level {part['clip']} (O-8 stopped at its deadline): "
+                         f"{d['m'] - part['live_edges']} of {d['m']} edges exact, the rest by properties "
+                         f"(kmax {kmax})")
         pytest.xfail(f"no exact trussness golden for this config (O-8 takes hours); T, every support and the "
                      f"trussness properties hold (kmax {kmax}, {np.unique(tau).size} levels)")
     for k in ks:
