@@ -132,8 +132,12 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "round2"))
+    ap.add_argument("--render", help="only re-render configs.md from this configs.jsonl")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
+    if a.render:
+        write_md([json.loads(ln) for ln in open(a.render) if ln.strip()], a.out)
+        return
     lines = []
     for name in a.configs.split(","):
         d = gpu_side(name, a.reps)
@@ -146,7 +150,11 @@ def main():
     with open(os.path.join(a.out, "configs.jsonl"), "w") as f:
         for d in lines:
             f.write(json.dumps(d) + "\n")
-    with open(os.path.join(a.out, "configs.md"), "w") as f:
+    write_md(lines, a.out)
+
+
+def write_md(lines, out):
+    with open(os.path.join(out, "configs.md"), "w") as f:
         f.write("# Per-config results (scripts/run_configs.py)\n\n")
         f.write("Device times: best of the runs, CUDA events inside libgc. Rates: m / kernel time.\n\n")
         f.write("| config | n | m | T | build ms | TC ms | TC edges/s | support ms | k=3..6 ms | decomposition | mem GB |\n")
@@ -162,7 +170,7 @@ def main():
             o = d.get("oracle")
             if not o:
                 continue
-            if "threads" in o:
+            if isinstance(o.get("threads"), dict):
                 for t, r in o["threads"].items():
                     f.write(f"| {d['config']} | {o['where']} ({o['cpu']}) | {t} | {r['canonicalize_adjacency_s']} | "
                             f"{r['support_s']} | {r['triangle_count_s']} | {r['tc_support_edges_per_s']:.3g} |\n")
