@@ -16,6 +16,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TIMEOUT_S = 300
 
 # name: (exact text in oracle.c, replacement).  Semantics-preserving edits
 # (e.g. never taking a galloping branch, not advancing past a match in a list
@@ -60,12 +61,16 @@ def run(name: str, src: str, old: str, new: str) -> bool:
         shutil.copy(os.path.join(ROOT, "Makefile"), tmp)
         open(os.path.join(tmp, "oracle", "oracle.c"), "w").write(src.replace(old, new))
         subprocess.run(["make", "-C", tmp, "gen", "oracle"], check=True, capture_output=True)
-        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:warnings", "-p", "no:cacheprovider",
-                            os.path.join(tmp, "tests", "test_oracle_pins.py")],
-                           cwd=tmp, capture_output=True, text=True,
-                           env={**os.environ, "PYTHONPATH": tmp})
-        killed = r.returncode != 0
-        last = [ln for ln in r.stdout.splitlines() if ln.strip()][-1:] or [""]
+        try:
+            r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:warnings", "-p",
+                                "no:cacheprovider", os.path.join(tmp, "tests", "test_oracle_pins.py")],
+                               cwd=tmp, capture_output=True, text=True, timeout=TIMEOUT_S,
+                               env={**os.environ, "PYTHONPATH": tmp})
+            killed = r.returncode != 0
+            last = [ln for ln in r.stdout.splitlines() if ln.strip()][-1:] or [""]
+        except subprocess.TimeoutExpired:
+            # a mutant that never terminates (e.g. x never leaves the graph) fails the pins too
+            killed, last = True, [f"no result after {TIMEOUT_S} s (the unmutated pins take under a minute)"]
         print(f"{name:28s} {'killed' if killed else 'SURVIVED'}  {last[0][:90]}", flush=True)
         return killed
 
